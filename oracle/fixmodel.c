@@ -1,0 +1,290 @@
+/*
+ * oracle/fixmodel.c -- bit-exact CPU model of the device arithmetic.
+ *
+ * TEST INFRASTRUCTURE ONLY (tests/ and smoke() use it as the checker; the
+ * product never links it). It restates, in plain C with exact __int128
+ * column sums, the fixed-point algorithm that the sm_100a kernel
+ * (paper_1908_09301_b200/csrc/taylor_kernel.cu) implements, so that every
+ * coefficient the GPU produces can be compared bit for bit. DESIGN.md §3
+ * is the normative description; in short:
+ *
+ *   digit radix B = 2^28; a value is X * 2^-F, F = 28*Lf, X = sum d_j B^j,
+ *   j = 0..Lf, signed digits with |d_j| < B all carrying the sign of X.
+ *   Coefficients are tau-scaled (a~_i = a_i tau^i), so the state update is
+ *   the exact sum of the coefficient rows.
+ *
+ *   tprod(A, C, T) = sum_{p+q >= T} a_p c_q B^(p+q-T)   (truncated product)
+ *   rnd(V)         = floor((V + B^2/2) / B^2)          (two guard digits)
+ *
+ *   order i:  S_p  = rnd( sum_k tprod(coef[j_p][i-k], coef[k_p][k], Lf-2) )
+ *             U_m  = rnd( [i==0] cst_m B^2 + sum_j tprod(lin[m][j], coef[j][i], Lf-2)
+ *                                          + sum_t tprod(q_t, S_{p_t}, Lf-2) )
+ *             coef[m][i+1] = rnd( tprod(U_m, Ctab[i], Lf+sc-2) ),
+ *   Ctab[i] = round(tau * 2^(F + 28 sc) / (i+1)) computed on the host.
+ *   state'[m] = RN_P( sum_i coef[m][i] )  (exact sum, then ties-to-even
+ *                 rounding to the reference precision P)
+ *
+ * Terms are grouped by equation in stored order like the reference's
+ * systems.py:31 QuadraticODESystem; pairs are distinct (j,k) in first
+ * appearance order (systems.py:64 product_pairs).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define RADIX_BITS 28
+#define RADIX ((int64_t)1 << RADIX_BITS)
+
+typedef __int128 i128;
+
+typedef struct {
+  int D, NT, NP, Lf, sc, order;
+  const int32_t *cst;  /* D x W */
+  const int32_t *lin;  /* D x D x W */
+  const int32_t *q;    /* NT x W */
+  const int32_t *ctab; /* order x W */
+  int teq[64], tj[64], tk[64], tpair[64], pj[64], pk[64];
+} model_t;
+
+#define W(M) ((M)->Lf + 1)
+
+/* columns c in [T, T+ncols): out[c-T] += sum_{p+q=c} a_p b_q */
+static void tprod_acc(const int32_t *a, const int32_t *b, int L, int T, i128 *col, int ncols) {
+  for (int p = 0; p < L; p++) {
+    if (!a[p]) continue;
+    int q0 = T - p;
+    if (q0 < 0) q0 = 0;
+    for (int q = q0; q < L; q++) {
+      int c = p + q - T;
+      if (c >= ncols) break;
+      col[c] += (i128)((int64_t)a[p] * (int64_t)b[q]);
+    }
+  }
+}
+
+/* V = sum col[c] B^c (exact), return digits of rnd(V) = floor((V + B^2/2)/B^2) in out[0..Lf];
+   returns 1 on overflow (result does not fit Lf+1 digits) */
+static int round_cols(const i128 *col, int ncols, int Lf, int32_t *out) {
+  /* normalize to digits in [0, B) with floor carries, keep the top carry */
+  i128 carry = 0;
+  int64_t dig[4096 + 8];
+  for (int c = 0; c < ncols; c++) {
+    i128 v = col[c] + carry;
+    i128 d = v & (RADIX - 1);
+    carry = (v - d) >> RADIX_BITS; /* exact floor division */
+    dig[c] = (int64_t)d;
+  }
+  /* add B^2/2: digit 1 gets B/2 */
+  i128 v = (i128)dig[1] + (RADIX / 2);
+  int64_t cin = (int64_t)(v >> RADIX_BITS);
+  dig[1] = (int64_t)(v & (RADIX - 1));
+  for (int c = 2; c < ncols && cin; c++) {
+    v = (i128)dig[c] + cin;
+    cin = (int64_t)(v >> RADIX_BITS);
+    dig[c] = (int64_t)(v & (RADIX - 1));
+  }
+  carry += cin;
+  /* result digits = dig[2..], value = sum dig[2+j] B^j + carry B^(ncols-2) (two's-complement-like) */
+  int nres = ncols - 2;
+  /* build signed result: if carry < 0 the number is negative; convert to sign-magnitude */
+  int neg = carry < 0;
+  int32_t mag[4096 + 8];
+  if (!neg) {
+    for (int j = 0; j < nres; j++) mag[j] = (int32_t)dig[2 + j];
+    if (carry != 0) return 1;
+  } else {
+    /* magnitude = -(value) = B^nres * (-carry) - sum dig B^j */
+    int64_t borrow = 0;
+    for (int j = 0; j < nres; j++) {
+      int64_t t = -dig[2 + j] - borrow;
+      if (t < 0) {
+        t += RADIX;
+        borrow = 1;
+      } else {
+        borrow = 0;
+      }
+      mag[j] = (int32_t)t;
+    }
+    /* remaining high part: -carry - borrow must be 0 */
+    if (-carry - borrow != 0) return 1;
+  }
+  for (int j = nres; j <= Lf; j++) mag[j] = 0;
+  for (int j = Lf + 1; j < nres; j++)
+    if (mag[j]) return 1;
+  for (int j = 0; j <= Lf; j++) out[j] = neg ? -mag[j] : mag[j];
+  return 0;
+}
+
+static int build(model_t *M, int D, int NT, const int32_t *teq, const int32_t *tj, const int32_t *tk) {
+  if (D > 16 || NT > 64) return -3;
+  M->D = D;
+  M->NT = NT;
+  M->NP = 0;
+  for (int t = 0; t < NT; t++) {
+    M->teq[t] = teq[t];
+    M->tj[t] = tj[t];
+    M->tk[t] = tk[t];
+    int p = -1;
+    for (int r = 0; r < M->NP; r++)
+      if (M->pj[r] == tj[t] && M->pk[r] == tk[t]) p = r;
+    if (p < 0) {
+      p = M->NP++;
+      M->pj[p] = tj[t];
+      M->pk[p] = tk[t];
+    }
+    M->tpair[t] = p;
+  }
+  return 0;
+}
+
+/* coef: D x (order+1) x W, coef[m][0] set by caller */
+static int jet(const model_t *M, int32_t *coef) {
+  int Lf = M->Lf, L = Lf + 1, Wd = W(M), D = M->D, N = M->order;
+  int ncols = Lf + 3; /* columns [Lf-2, 2Lf] */
+  i128 *col = malloc(sizeof(i128) * (size_t)(ncols + 2));
+  int32_t *S = malloc(sizeof(int32_t) * (size_t)(M->NP + 1) * Wd);
+  int32_t *U = malloc(sizeof(int32_t) * (size_t)D * Wd);
+  int rc = 0;
+#define CO(m, i) (coef + ((size_t)(m) * (N + 1) + (i)) * Wd)
+  for (int i = 0; i < N && !rc; i++) {
+    for (int p = 0; p < M->NP; p++) {
+      memset(col, 0, sizeof(i128) * ncols);
+      for (int k = 0; k <= i; k++) tprod_acc(CO(M->pj[p], i - k), CO(M->pk[p], k), L, Lf - 2, col, ncols);
+      if (round_cols(col, ncols, Lf, S + (size_t)p * Wd)) rc = 1;
+    }
+    for (int m = 0; m < D; m++) {
+      memset(col, 0, sizeof(i128) * ncols);
+      if (i == 0)
+        for (int j = 0; j <= Lf; j++) col[2 + j] += (i128)M->cst[(size_t)m * Wd + j];
+      for (int j = 0; j < D; j++) tprod_acc(M->lin + ((size_t)m * D + j) * Wd, CO(j, i), L, Lf - 2, col, ncols);
+      for (int t = 0; t < M->NT; t++)
+        if (M->teq[t] == m) tprod_acc(M->q + (size_t)t * Wd, S + (size_t)M->tpair[t] * Wd, L, Lf - 2, col, ncols);
+      if (round_cols(col, ncols, Lf, U + (size_t)m * Wd)) rc = 1;
+    }
+    for (int m = 0; m < D; m++) {
+      memset(col, 0, sizeof(i128) * ncols);
+      tprod_acc(U + (size_t)m * Wd, M->ctab + (size_t)i * Wd, L, Lf + M->sc - 2, col, ncols);
+      if (round_cols(col, ncols, Lf, CO(m, i + 1))) rc = 1;
+    }
+  }
+  free(col);
+  free(S);
+  free(U);
+  return rc;
+}
+
+/* round the canonical digit vector to `prec` significant bits, ties to even */
+static int round_prec(int32_t *d, int W, int prec) {
+  int tp = -1;
+  for (int j = W - 1; j >= 0; j--)
+    if (d[j]) { tp = j; break; }
+  if (tp < 0) return 0;
+  int neg = d[tp] < 0;
+  i128 mag = 0;  /* not big enough in general: work digit-wise */
+  (void)mag;
+  int64_t m[4096 + 8];
+  for (int j = 0; j < W; j++) m[j] = d[j] < 0 ? -(int64_t)d[j] : d[j];
+  int tb = 0;
+  while ((m[tp] >> tb) != 0) tb++;
+  int nbits = RADIX_BITS * tp + tb;
+  int s = nbits - prec;
+  if (s <= 0) return 0;
+  int sd = s / RADIX_BITS, sb = s % RADIX_BITS;
+  int hp = s - 1, hd = hp / RADIX_BITS, hb = hp % RADIX_BITS;
+  int half = (int)((m[hd] >> hb) & 1);
+  int lsb = (int)((m[sd] >> sb) & 1);
+  int sticky = (m[hd] & (((int64_t)1 << hb) - 1)) != 0;
+  for (int j = 0; j < hd; j++) sticky |= m[j] != 0;
+  for (int j = 0; j < sd; j++) m[j] = 0;
+  m[sd] &= ~(((int64_t)1 << sb) - 1);
+  if (half && (sticky || lsb)) {
+    int64_t cin = (int64_t)1 << sb;
+    for (int j = sd; j < W && cin; j++) {
+      m[j] += cin;
+      cin = m[j] >> RADIX_BITS;
+      m[j] &= RADIX - 1;
+    }
+    if (cin) return 1;
+  }
+  for (int j = 0; j < W; j++) d[j] = (int32_t)(neg ? -m[j] : m[j]);
+  return 0;
+}
+
+/* exact sum of the rows: state[m] = sum_i coef[m][i] */
+static int sum_rows(const model_t *M, const int32_t *coef, int32_t *state, int prec) {
+  int Lf = M->Lf, Wd = W(M), N = M->order;
+  i128 col[4096 + 8];
+  int rc = 0;
+  for (int m = 0; m < M->D; m++) {
+    /* reuse round_cols with two zero guard columns in front */
+    memset(col, 0, sizeof(i128) * (Wd + 3));
+    for (int i = 0; i <= N; i++)
+      for (int j = 0; j <= Lf; j++) col[2 + j] += (i128)coef[((size_t)m * (N + 1) + i) * Wd + j];
+    if (round_cols(col, Wd + 3, Lf, state + (size_t)m * Wd)) rc = 1;
+    if (round_prec(state + (size_t)m * Wd, Wd, prec)) rc = 1;
+  }
+  return rc;
+}
+
+int fix_compute_jet(int D, int NT, const int32_t *teq, const int32_t *tj, const int32_t *tk, int Lf,
+                    int sc, int order, const int32_t *cst, const int32_t *lin, const int32_t *q,
+                    const int32_t *ctab, const int32_t *state, int32_t *coef_out) {
+  model_t M;
+  int rc = build(&M, D, NT, teq, tj, tk);
+  if (rc) return rc;
+  if (Lf + 4 > 4096) return -4;
+  M.Lf = Lf;
+  M.sc = sc;
+  M.order = order;
+  M.cst = cst;
+  M.lin = lin;
+  M.q = q;
+  M.ctab = ctab;
+  int Wd = Lf + 1;
+  for (int m = 0; m < D; m++)
+    memcpy(coef_out + (size_t)m * (order + 1) * Wd, state + (size_t)m * Wd, sizeof(int32_t) * Wd);
+  return jet(&M, coef_out);
+}
+
+/* records: step start, every multiple of stride, and n_steps; returns #records or <0 */
+int fix_integrate(int D, int NT, const int32_t *teq, const int32_t *tj, const int32_t *tk, int Lf,
+                  int sc, int order, int prec, const int32_t *cst, const int32_t *lin, const int32_t *q,
+                  const int32_t *ctab, const int32_t *state0, int n_steps, int start_step,
+                  int stride, int max_rec, int32_t *rec_step, int32_t *rec_state) {
+  model_t M;
+  int rc = build(&M, D, NT, teq, tj, tk);
+  if (rc) return rc;
+  if (Lf + 4 > 4096) return -4;
+  M.Lf = Lf;
+  M.sc = sc;
+  M.order = order;
+  M.cst = cst;
+  M.lin = lin;
+  M.q = q;
+  M.ctab = ctab;
+  int Wd = Lf + 1;
+  int32_t *coef = malloc(sizeof(int32_t) * (size_t)D * (order + 1) * Wd);
+  int32_t *state = malloc(sizeof(int32_t) * (size_t)D * Wd);
+  memcpy(state, state0, sizeof(int32_t) * (size_t)D * Wd);
+  int nrec = 0;
+  rc = 0;
+  if (max_rec < 1) { rc = -2; goto out; }
+  rec_step[nrec] = start_step;
+  memcpy(rec_state, state, sizeof(int32_t) * (size_t)D * Wd);
+  nrec++;
+  for (int n = start_step + 1; n <= n_steps; n++) {
+    for (int m = 0; m < D; m++)
+      memcpy(coef + (size_t)m * (order + 1) * Wd, state + (size_t)m * Wd, sizeof(int32_t) * Wd);
+    if (jet(&M, coef) || sum_rows(&M, coef, state, prec)) { rc = -1; goto out; }
+    if (n % stride == 0 || n == n_steps) {
+      if (nrec >= max_rec) { rc = -2; goto out; }
+      rec_step[nrec] = n;
+      memcpy(rec_state + (size_t)nrec * D * Wd, state, sizeof(int32_t) * (size_t)D * Wd);
+      nrec++;
+    }
+  }
+out:
+  free(coef);
+  free(state);
+  return rc < 0 ? rc : nrec;
+}

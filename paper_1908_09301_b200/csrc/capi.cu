@@ -1,0 +1,357 @@
+// C ABI of the B200 Taylor engine: plan construction, constant upload,
+// launches. See include/mptaylor_b200.h for the contract.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mptaylor_b200.h"
+#include "mpt_common.cuh"
+
+namespace mpt {
+size_t smem_bytes(const Params& p);
+cudaError_t launch_team_kernel(const Params& p, size_t smem, cudaStream_t stream);
+}  // namespace mpt
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(MPT_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+struct mpt_plan {
+  mpt::Params p;
+  int device = 0;
+  int W = 0;
+  size_t smem = 0;
+  int32_t *d_cst = nullptr, *d_lin = nullptr, *d_q = nullptr, *d_ctab = nullptr;
+  int32_t *d_coef = nullptr, *d_state = nullptr, *d_rec = nullptr, *d_status = nullptr;
+  int2* d_rinfo = nullptr;
+  size_t rec_slots = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  float last_ms = 0.f;
+  bool have_constants = false;
+};
+
+extern "C" {
+
+int mpt_version(void) { return 1; }
+const char* mpt_last_error(void) { return g_err.c_str(); }
+
+int mpt_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int mpt_record_count(int n_steps, int start_step, int stride) {
+  if (stride < 1 || n_steps < start_step) return MPT_EINVAL;
+  int n = 1 + (n_steps / stride - start_step / stride);
+  if (n_steps % stride) n += 1;
+  return n;
+}
+
+int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq, const int32_t* term_j,
+                    const int32_t* term_k, int frac_digits, int c_shift, int order, int prec_bits,
+                    int n_traj, int device) {
+  if (!out) return fail(MPT_EINVAL, "null plan pointer");
+  *out = nullptr;
+  if (mpt_device_count() <= 0) return fail(MPT_ENODEV, "no CUDA device available");
+  if (dim < 1 || dim > mpt::kMaxD) return fail(MPT_EUNSUP, "dim must be in [1, 4] on the device");
+  if (nterms < 0 || nterms > mpt::kMaxT) return fail(MPT_EUNSUP, "too many bilinear terms");
+  if (frac_digits < 3 || order < 1 || n_traj < 1 || (c_shift != 0 && c_shift != 1) || prec_bits < 1)
+    return fail(MPT_EINVAL, "invalid plan dimensions");
+  if (frac_digits + 4 > 32 * mpt::kMaxLanesDigits - 8)
+    return fail(MPT_EUNSUP, "precision too large for the device normaliser");
+  mpt_plan* pl = new mpt_plan();
+  mpt::Params& p = pl->p;
+  std::memset(&p, 0, sizeof(p));
+  p.D = dim;
+  p.NT = nterms;
+  p.Lf = frac_digits;
+  p.W = frac_digits + 1;
+  p.RS = (p.W + 3) / 4 * 4;
+  p.sc = c_shift;
+  p.N = order;
+  p.P = prec_bits;
+  p.n_traj = n_traj;
+  p.nthreads = 256;
+  // distinct pairs in first-appearance order (systems.py:64 product_pairs)
+  for (int t = 0; t < nterms; t++) {
+    if (term_eq[t] < 0 || term_eq[t] >= dim || term_j[t] < 0 || term_k[t] < term_j[t] || term_k[t] >= dim) {
+      delete pl;
+      return fail(MPT_EINVAL, "bad bilinear term indices");
+    }
+    int q = -1;
+    for (int r = 0; r < p.NP; r++)
+      if (p.pj[r] == term_j[t] && p.pk[r] == term_k[t]) q = r;
+    if (q < 0) {
+      if (p.NP >= mpt::kMaxP) {
+        delete pl;
+        return fail(MPT_EUNSUP, "too many distinct product pairs");
+      }
+      q = p.NP++;
+      p.pj[q] = term_j[t];
+      p.pk[q] = term_k[t];
+    }
+    p.teq[t] = term_eq[t];
+    p.tpair[t] = q;
+  }
+  for (int q = 0; q < p.NP; q++) {
+    int a = -1, b = -1;
+    for (int v = 0; v < p.nlv; v++)
+      if (p.lvar[v] == p.pj[q]) a = v;
+    if (a < 0) {
+      a = p.nlv++;
+      p.lvar[a] = p.pj[q];
+    }
+    for (int v = 0; v < p.nrv; v++)
+      if (p.rvar[v] == p.pk[q]) b = v;
+    if (b < 0) {
+      b = p.nrv++;
+      p.rvar[b] = p.pk[q];
+    }
+    p.pl[q] = a;
+    p.pr[q] = b;
+  }
+  pl->device = device;
+  pl->W = p.W;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    delete pl;
+    return fail(MPT_ENODEV, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  }
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  // largest k-chunk that fits in shared memory
+  size_t smem = 0;
+  int kc = 64;
+  for (; kc >= 1; kc = kc > 8 ? kc - 8 : kc - 1) {
+    p.kc = kc;
+    smem = mpt::smem_bytes(p);
+    if (smem <= (size_t)optin) break;
+  }
+  if (kc < 1) {
+    delete pl;
+    return fail(MPT_EUNSUP, "shared memory budget exceeded");
+  }
+  pl->smem = smem;
+  size_t rows = (size_t)n_traj * dim * (order + 1);
+#define ALLOC(ptr, bytes)                                                         \
+  do {                                                                            \
+    e = cudaMalloc((void**)&(ptr), (bytes));                                      \
+    if (e != cudaSuccess) {                                                       \
+      mpt_plan_destroy(pl);                                                       \
+      return fail(MPT_ECUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e)); \
+    }                                                                             \
+  } while (0)
+  ALLOC(pl->d_cst, sizeof(int32_t) * (size_t)dim * p.RS);
+  ALLOC(pl->d_lin, sizeof(int32_t) * (size_t)dim * dim * p.RS);
+  ALLOC(pl->d_q, sizeof(int32_t) * (size_t)(nterms > 0 ? nterms : 1) * p.RS);
+  ALLOC(pl->d_ctab, sizeof(int32_t) * (size_t)order * p.RS);
+  ALLOC(pl->d_coef, sizeof(int32_t) * rows * p.RS);
+  ALLOC(pl->d_rinfo, sizeof(int2) * rows);
+  ALLOC(pl->d_state, sizeof(int32_t) * (size_t)n_traj * dim * p.RS);
+  ALLOC(pl->d_status, sizeof(int32_t) * (size_t)n_traj);
+  cudaMemset(pl->d_state, 0, sizeof(int32_t) * (size_t)n_traj * dim * p.RS);
+  cudaMemset(pl->d_coef, 0, sizeof(int32_t) * rows * p.RS);
+  cudaEventCreate(&pl->ev0);
+  cudaEventCreate(&pl->ev1);
+  p.cst = pl->d_cst;
+  p.lin = pl->d_lin;
+  p.q = pl->d_q;
+  p.ctab = pl->d_ctab;
+  p.coef = pl->d_coef;
+  p.rinfo = pl->d_rinfo;
+  p.state = pl->d_state;
+  p.status = pl->d_status;
+  *out = pl;
+  return MPT_OK;
+}
+
+int mpt_plan_destroy(mpt_plan* pl) {
+  if (!pl) return MPT_OK;
+  cudaFree(pl->d_cst);
+  cudaFree(pl->d_lin);
+  cudaFree(pl->d_q);
+  cudaFree(pl->d_ctab);
+  cudaFree(pl->d_coef);
+  cudaFree(pl->d_rinfo);
+  cudaFree(pl->d_state);
+  cudaFree(pl->d_rec);
+  cudaFree(pl->d_status);
+  if (pl->ev0) cudaEventDestroy(pl->ev0);
+  if (pl->ev1) cudaEventDestroy(pl->ev1);
+  delete pl;
+  return MPT_OK;
+}
+
+int mpt_plan_width(const mpt_plan* pl) { return pl ? pl->W : MPT_EINVAL; }
+
+int mpt_plan_info(const mpt_plan* pl, int* smem_bytes, int* k_chunk, int* threads) {
+  if (!pl) return MPT_EINVAL;
+  if (smem_bytes) *smem_bytes = (int)pl->smem;
+  if (k_chunk) *k_chunk = pl->p.kc;
+  if (threads) *threads = pl->p.nthreads;
+  return MPT_OK;
+}
+
+// host values (W digits each) -> device rows (RS stride)
+static int upload_rows(int32_t* dst, const int32_t* src, size_t nvals, int W, int RS) {
+  std::vector<int32_t> buf(nvals * RS, 0);
+  for (size_t v = 0; v < nvals; v++) std::memcpy(&buf[v * RS], src + v * W, sizeof(int32_t) * W);
+  CK(cudaMemcpy(dst, buf.data(), sizeof(int32_t) * buf.size(), cudaMemcpyHostToDevice));
+  return MPT_OK;
+}
+
+static int download_rows(int32_t* dst, const int32_t* src, size_t nvals, int W, int RS) {
+  std::vector<int32_t> buf(nvals * RS);
+  CK(cudaMemcpy(buf.data(), src, sizeof(int32_t) * buf.size(), cudaMemcpyDeviceToHost));
+  for (size_t v = 0; v < nvals; v++) std::memcpy(dst + v * W, &buf[v * RS], sizeof(int32_t) * W);
+  return MPT_OK;
+}
+
+int mpt_plan_set_constants(mpt_plan* pl, const int32_t* cst, const int32_t* lin, const int32_t* q,
+                           const int32_t* ctab) {
+  if (!pl || !cst || !lin || !ctab || (pl->p.NT > 0 && !q)) return fail(MPT_EINVAL, "null constant table");
+  CK(cudaSetDevice(pl->device));
+  const mpt::Params& p = pl->p;
+  int rc;
+  if ((rc = upload_rows(pl->d_cst, cst, p.D, p.W, p.RS))) return rc;
+  if ((rc = upload_rows(pl->d_lin, lin, (size_t)p.D * p.D, p.W, p.RS))) return rc;
+  if (p.NT > 0 && (rc = upload_rows(pl->d_q, q, p.NT, p.W, p.RS))) return rc;
+  if ((rc = upload_rows(pl->d_ctab, ctab, p.N, p.W, p.RS))) return rc;
+  pl->have_constants = true;
+  return MPT_OK;
+}
+
+static int ensure_rec(mpt_plan* pl, size_t slots) {
+  if (slots <= pl->rec_slots) return MPT_OK;
+  cudaFree(pl->d_rec);
+  pl->d_rec = nullptr;
+  CK(cudaMalloc((void**)&pl->d_rec, sizeof(int32_t) * slots * pl->p.n_traj * pl->p.D * pl->p.RS));
+  pl->rec_slots = slots;
+  return MPT_OK;
+}
+
+static int launch(mpt_plan* pl, int n_steps, int start_step, int stride, cudaStream_t stream) {
+  mpt::Params p = pl->p;
+  p.n_steps = n_steps;
+  p.start_step = start_step;
+  p.stride = stride;
+  p.rec = pl->d_rec;
+  CK(cudaEventRecord(pl->ev0, stream));
+  CK(mpt::launch_team_kernel(p, pl->smem, stream));
+  CK(cudaEventRecord(pl->ev1, stream));
+  return MPT_OK;
+}
+
+static int finish(mpt_plan* pl, cudaStream_t stream, int32_t* status) {
+  CK(cudaStreamSynchronize(stream));
+  CK(cudaGetLastError());
+  cudaEventElapsedTime(&pl->last_ms, pl->ev0, pl->ev1);
+  if (status) CK(cudaMemcpy(status, pl->d_status, sizeof(int32_t) * pl->p.n_traj, cudaMemcpyDeviceToHost));
+  return MPT_OK;
+}
+
+int mpt_state_upload(mpt_plan* pl, const int32_t* state0) {
+  if (!pl || !state0) return fail(MPT_EINVAL, "null argument");
+  CK(cudaSetDevice(pl->device));
+  return upload_rows(pl->d_state, state0, (size_t)pl->p.n_traj * pl->p.D, pl->p.W, pl->p.RS);
+}
+
+int mpt_state_download(mpt_plan* pl, int32_t* state) {
+  if (!pl || !state) return fail(MPT_EINVAL, "null argument");
+  CK(cudaSetDevice(pl->device));
+  return download_rows(state, pl->d_state, (size_t)pl->p.n_traj * pl->p.D, pl->p.W, pl->p.RS);
+}
+
+int mpt_integrate(mpt_plan* pl, const int32_t* state0, int n_steps, int start_step, int stride,
+                  int32_t* rec_steps, int32_t* records, int32_t* status) {
+  if (!pl || !state0 || !records || !rec_steps) return fail(MPT_EINVAL, "null argument");
+  if (!pl->have_constants) return fail(MPT_EINVAL, "constants not set");
+  int nrec = mpt_record_count(n_steps, start_step, stride);
+  if (nrec < 1 || start_step < 0) return fail(MPT_EINVAL, "invalid step range");
+  CK(cudaSetDevice(pl->device));
+  int rc;
+  if ((rc = ensure_rec(pl, nrec))) return rc;
+  if ((rc = mpt_state_upload(pl, state0))) return rc;
+  cudaStream_t s = 0;
+  if (n_steps > start_step) {
+    if ((rc = launch(pl, n_steps, start_step, stride, s))) return rc;
+    if ((rc = finish(pl, s, status))) return rc;
+  } else if (status) {
+    std::memset(status, 0, sizeof(int32_t) * pl->p.n_traj);
+  }
+  const mpt::Params& p = pl->p;
+  size_t per = (size_t)p.n_traj * p.D;
+  std::memcpy(records, state0, sizeof(int32_t) * per * p.W);
+  if (nrec > 1 && (rc = download_rows(records + per * p.W, pl->d_rec + per * p.RS, per * (nrec - 1), p.W, p.RS)))
+    return rc;
+  int r = 0;
+  rec_steps[r++] = start_step;
+  for (int n = start_step + 1; n <= n_steps; n++)
+    if (n % stride == 0 || n == n_steps) rec_steps[r++] = n;
+  if (status)
+    for (int t = 0; t < p.n_traj; t++)
+      if (status[t]) return fail(MPT_ERANGE, "fixed-point range exceeded on the device");
+  return nrec;
+}
+
+int mpt_integrate_device(mpt_plan* pl, int n_steps, void* stream) {
+  if (!pl || !pl->have_constants) return fail(MPT_EINVAL, "plan not ready");
+  CK(cudaSetDevice(pl->device));
+  int rc;
+  // records are only written for multiples of `stride`: use a stride beyond n_steps
+  if ((rc = ensure_rec(pl, 2))) return rc;
+  return launch(pl, n_steps, 0, n_steps + 1, (cudaStream_t)stream);
+}
+
+int mpt_compute_jet(mpt_plan* pl, const int32_t* state, int32_t* coef, int32_t* status) {
+  if (!pl || !state || !coef) return fail(MPT_EINVAL, "null argument");
+  if (!pl->have_constants) return fail(MPT_EINVAL, "constants not set");
+  CK(cudaSetDevice(pl->device));
+  int rc;
+  if ((rc = ensure_rec(pl, 2))) return rc;
+  if ((rc = mpt_state_upload(pl, state))) return rc;
+  if ((rc = launch(pl, 1, 0, 2, 0))) return rc;
+  if ((rc = finish(pl, 0, status))) return rc;
+  const mpt::Params& p = pl->p;
+  if ((rc = download_rows(coef, pl->d_coef, (size_t)p.n_traj * p.D * (p.N + 1), p.W, p.RS))) return rc;
+  if (status)
+    for (int t = 0; t < p.n_traj; t++)
+      if (status[t]) return fail(MPT_ERANGE, "fixed-point range exceeded on the device");
+  return MPT_OK;
+}
+
+int mpt_step(mpt_plan* pl, const int32_t* state, int32_t* state_out, int32_t* status) {
+  if (!pl || !state || !state_out) return fail(MPT_EINVAL, "null argument");
+  CK(cudaSetDevice(pl->device));
+  int rc;
+  if ((rc = ensure_rec(pl, 2))) return rc;
+  if ((rc = mpt_state_upload(pl, state))) return rc;
+  if ((rc = launch(pl, 1, 0, 2, 0))) return rc;
+  if ((rc = finish(pl, 0, status))) return rc;
+  if ((rc = mpt_state_download(pl, state_out))) return rc;
+  if (status)
+    for (int t = 0; t < pl->p.n_traj; t++)
+      if (status[t]) return fail(MPT_ERANGE, "fixed-point range exceeded on the device");
+  return MPT_OK;
+}
+
+float mpt_last_kernel_ms(const mpt_plan* pl) { return pl ? pl->last_ms : -1.f; }
+
+}  // extern "C"

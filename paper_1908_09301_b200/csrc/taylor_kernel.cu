@@ -1,0 +1,628 @@
+// Persistent multiple-precision Taylor kernel for sm_100a.
+//
+// One CTA owns one trajectory for the whole launch: it loops over steps and,
+// inside each step, over the Taylor orders i = 0..N-1 of the recurrence
+// (reference taylor.py:148 _jet_rows, paper Eq. (3)), with __syncthreads()
+// between phases instead of kernel relaunches. Per order:
+//
+//   phase A  Cauchy sums  S_p = sum_k coef[j_p][i-k] (x) coef[k_p][k]
+//            column-wise in exact 64-bit integer accumulators (IMAD.WIDE),
+//            rows staged in shared memory, leading/trailing zero digits
+//            skipped, ONE carry propagation + rounding per sum.
+//   phase B  numerators U_m = [i==0] c_m + sum_j L_mj (x) coef[j][i]
+//                             + sum_t q_t (x) S_{p_t}
+//   phase C  coef[m][i+1] = U_m (x) tau/(i+1)       (the 1/(i+1) scaling)
+//
+// and after the last order the state update x_{n+1} = sum_i coef[i] (the
+// tau-scaled Horner evaluation, reference taylor.py:187) followed by the
+// rounding of the state to the reference precision P (round-to-nearest-even).
+// oracle/fixmodel.c restates exactly this arithmetic on the CPU.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "mpt_common.cuh"
+
+namespace mpt {
+
+__host__ __device__ inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+__host__ __device__ inline int row_words(int RS) { return RS + 2 * kPad; }
+
+struct Geo {
+  int Tb, gfb, NGb;  // base products: first column, first group, #groups
+  int Tc, gfc, NGc;  // tau/(i+1) products
+  int NCX;           // column-sum length (relative to T), covers all groups + carry
+};
+
+__host__ __device__ inline Geo make_geo(const Params& p) {
+  Geo g;
+  g.Tb = p.Lf - 2;
+  g.gfb = g.Tb / kR;
+  g.NGb = (2 * p.Lf) / kR - g.gfb + 1;
+  g.Tc = p.Lf + p.sc - 2;
+  g.gfc = g.Tc / kR;
+  g.NGc = (2 * p.Lf) / kR - g.gfc + 1;
+  g.NCX = kR * (g.NGb + 2);
+  return g;
+}
+
+// Shared-memory carve-up (identical on host and device).
+struct Layout {
+  int rw;                 // words per staged row
+  int n_stage_rows;       // kc * (nlv + nrv)
+  int n_const_rows;       // D + D*D + NT
+  int n_units;            // partial-sum units
+  size_t off_stage, off_sinfo, off_const, off_cinfo, off_cur, off_curinfo, off_s, off_sinf,
+      off_u, off_uinf, off_ct, off_ctinf, off_part, off_col, off_uout, off_flag, total;
+};
+
+__host__ __device__ inline Layout make_layout(const Params& p) {
+  Geo g = make_geo(p);
+  Layout L;
+  L.rw = row_words(p.RS);
+  L.n_stage_rows = p.kc * (p.nlv + p.nrv);
+  L.n_const_rows = p.D + p.D * p.D + p.NT;
+  int ns = p.nthreads / g.NGb;
+  if (ns < 1) ns = 1;
+  int units_a = ns * (p.NP > 0 ? p.NP : 1);
+  int units_b = p.D * p.D + p.NT;  // numerator items
+  int units_c = p.D;
+  int u = units_a;
+  if (units_b > u) u = units_b;
+  if (units_c > u) u = units_c;
+  L.n_units = u;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t r = o;
+    o += (bytes + 15) / 16 * 16;
+    return r;
+  };
+  L.off_stage = take(sizeof(int32_t) * (size_t)L.n_stage_rows * L.rw);
+  L.off_sinfo = take(sizeof(int2) * (size_t)L.n_stage_rows);
+  L.off_const = take(sizeof(int32_t) * (size_t)L.n_const_rows * L.rw);
+  L.off_cinfo = take(sizeof(int2) * (size_t)L.n_const_rows);
+  L.off_cur = take(sizeof(int32_t) * (size_t)p.D * L.rw);
+  L.off_curinfo = take(sizeof(int2) * (size_t)p.D);
+  L.off_s = take(sizeof(int32_t) * (size_t)(p.NP > 0 ? p.NP : 1) * L.rw);
+  L.off_sinf = take(sizeof(int2) * (size_t)(p.NP > 0 ? p.NP : 1));
+  L.off_u = take(sizeof(int32_t) * (size_t)p.D * L.rw);
+  L.off_uinf = take(sizeof(int2) * (size_t)p.D);
+  L.off_ct = take(sizeof(int32_t) * (size_t)L.rw);
+  L.off_ctinf = take(sizeof(int2));
+  L.off_part = take(sizeof(int64_t) * (size_t)L.n_units * g.NCX);
+  int nout = p.NP > p.D ? p.NP : p.D;
+  L.off_col = take(sizeof(int64_t) * (size_t)nout * g.NCX);
+  L.off_uout = take(sizeof(int) * (size_t)L.n_units);
+  L.off_flag = take(sizeof(int) * 4);
+  L.total = o;
+  return L;
+}
+
+// ---------------------------------------------------------------------------
+// Column accumulation for one (operand pair, column group).
+// acc[r] += sum_p A[p] * B[c0 + r - p] for the group's absolute columns
+// c0..c0+kR-1; acc[kR] collects the carries of folds. Rows are padded with
+// kPad zeros on both sides so the register window never needs bounds checks.
+struct Acc {
+  int64_t v[kR + 1];
+};
+
+__device__ __forceinline__ void acc_zero(Acc& a) {
+#pragma unroll
+  for (int r = 0; r <= kR; r++) a.v[r] = 0;
+}
+
+// fold: digits of acc[0..kR-1] into [0, B), carries ripple upward into acc[kR].
+// Columns below `tcut` (absolute) are discarded first: products there are
+// outside the truncated product and must not leak carries upward.
+__device__ __forceinline__ void acc_fold(Acc& a, int c0, int tcut) {
+#pragma unroll
+  for (int r = 0; r < kR; r++) {
+    if (c0 + r < tcut) a.v[r] = 0;
+    int64_t c = a.v[r] >> kRadixBits;
+    a.v[r] &= kMask;
+    a.v[r + 1] += c;
+  }
+}
+
+__device__ __forceinline__ void mac_group(Acc& acc, int& cnt, const int32_t* __restrict__ A, int2 ia,
+                                          const int32_t* __restrict__ B, int2 ib, int c0, int tcut) {
+  // nonzero digits: A in [ia.x, ia.y], B in [ib.x, ib.y]
+  int plo = max(ia.x, c0 - ib.y);
+  int phi = min(ia.y, c0 + kR - 1 - ib.x);
+  if (plo > phi) return;
+  int P0 = plo & ~(kR - 1);
+  int32_t buf[kR];
+  const int32_t* bq = B + (c0 - P0);  // bq[s] = B[c0 - P0 + s]
+#pragma unroll
+  for (int s = 1; s < kR; s++) buf[s] = bq[s];
+  for (; P0 <= phi; P0 += kR) {
+    const int32_t* ap = A + P0;
+    const int32_t* bp = B + (c0 - P0);
+#pragma unroll
+    for (int u = 0; u < kR; u++) {
+      buf[(kR - u) & (kR - 1)] = bp[-u];
+      int64_t a = ap[u];
+#pragma unroll
+      for (int r = 0; r < kR; r++) acc.v[r] += a * (int64_t)buf[(r - u) & (kR - 1)];
+    }
+    cnt += kR;
+    if (cnt >= kFoldEvery) {
+      acc_fold(acc, c0, tcut);
+      cnt = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-cooperative normalisation of a column vector (relative columns
+// 0..ncols-1, value V = sum col[c] B^c) into canonical signed digits of
+// floor((V + shift_half) / B^drop), drop in {0, 2}. Output digits j = 0..W-1
+// go to `out` (a padded shared row), bot/top of nonzero digits to *info.
+// Returns true on overflow. Runs on one full warp.
+__device__ __forceinline__ void warp_carry(int64_t (&v)[kMaxLanesDigits], int m, int64_t& top) {
+  const unsigned full = 0xffffffffu;
+  int lane = threadIdx.x & 31;
+  int64_t c = 0;
+#pragma unroll
+  for (int j = 0; j < kMaxLanesDigits; j++) {
+    if (j < m) {
+      int64_t t = v[j] + c;
+      int64_t d = t & kMask;
+      c = (t - d) >> kRadixBits;
+      v[j] = d;
+    }
+  }
+  while (__any_sync(full, c != 0)) {
+    int64_t cin = __shfl_up_sync(full, c, 1);
+    if (lane == 0) cin = 0;
+    if (lane == 31) top += c;
+    c = 0;
+    if (cin != 0) {
+#pragma unroll
+      for (int j = 0; j < kMaxLanesDigits; j++) {
+        if (j < m) {
+          int64_t t = v[j] + cin;
+          int64_t d = t & kMask;
+          cin = (t - d) >> kRadixBits;
+          v[j] = d;
+        }
+      }
+      c = cin;
+    }
+  }
+  top = __shfl_sync(full, top, 31);
+}
+
+__device__ void round_to_prec(int32_t* out, int W, int prec_bits, bool& ovf) {
+  // lane-0 sequential: round the canonical digit vector to prec_bits
+  // significant bits, ties to even (the reference's state precision).
+  int tp = -1;
+  for (int d = W - 1; d >= 0; d--)
+    if (out[d]) {
+      tp = d;
+      break;
+    }
+  if (tp < 0) return;
+  const bool neg = out[tp] < 0;
+  auto mag = [&](int d) -> int32_t { return out[d] < 0 ? -out[d] : out[d]; };
+  const int nbits = kRadixBits * tp + (32 - __clz(mag(tp)));
+  const int s = nbits - prec_bits;  // number of low bits to drop
+  if (s <= 0) return;
+  const int sd = s / kRadixBits, sb = s % kRadixBits;
+  const int hp = s - 1, hd = hp / kRadixBits, hb = hp % kRadixBits;
+  const bool half = (mag(hd) >> hb) & 1;
+  const bool lsb = (mag(sd) >> sb) & 1;
+  bool sticky = (mag(hd) & ((1 << hb) - 1)) != 0;
+  for (int d = 0; d < hd && !sticky; d++) sticky = out[d] != 0;
+  for (int d = 0; d < sd; d++) out[d] = 0;
+  int64_t m = mag(sd) & ~((int64_t(1) << sb) - 1);
+  int64_t cin = (half && (sticky || lsb)) ? (int64_t(1) << sb) : 0;
+  for (int d = sd; d < W; d++) {
+    if (d > sd) {
+      if (!cin) break;
+      m = mag(d);
+    }
+    m += cin;
+    cin = m >> kRadixBits;
+    m &= kMask;
+    out[d] = (int32_t)(neg ? -m : m);
+  }
+  if (cin) ovf = true;
+}
+
+__device__ bool warp_normalize(const int64_t* col, int ncols, int drop, int W, int32_t* out, int2* info,
+                               int round_prec_bits) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int m = (ncols + 31) / 32;
+  int64_t v[kMaxLanesDigits];
+#pragma unroll
+  for (int j = 0; j < kMaxLanesDigits; j++) {
+    int c = lane * m + j;
+    v[j] = (j < m && c < ncols) ? col[c] : 0;
+  }
+  int64_t top = 0;
+  warp_carry(v, m, top);  // digits in [0, B), signed carry in `top`
+  if (drop) {
+    // floor((V + B^drop/2) / B^drop): add B/2 at column drop-1, propagate,
+    // then discard the (non-negative) low digits.
+#pragma unroll
+    for (int j = 0; j < kMaxLanesDigits; j++)
+      if (lane * m + j == drop - 1) v[j] += kRadix / 2;
+    warp_carry(v, m, top);
+#pragma unroll
+    for (int j = 0; j < kMaxLanesDigits; j++)
+      if (lane * m + j < drop) v[j] = 0;
+  }
+  const bool neg = top < 0;
+  if (neg) {  // magnitude of a negative result: negate and renormalise
+#pragma unroll
+    for (int j = 0; j < kMaxLanesDigits; j++) v[j] = -v[j];
+    top = -top;
+    warp_carry(v, m, top);
+  }
+  bool ovf = top != 0;
+#pragma unroll
+  for (int j = 0; j < kMaxLanesDigits; j++) {
+    int c = lane * m + j;
+    if (j < m && c >= drop && c < ncols) {
+      int d = c - drop;
+      int32_t dig = (int32_t)v[j];
+      if (d < W)
+        out[d] = neg ? -dig : dig;
+      else if (dig)
+        ovf = true;
+    }
+  }
+  for (int d = ncols - drop + lane; d < W; d += 32) out[d] = 0;
+  ovf = __any_sync(full, ovf);
+  __syncwarp();
+  if (round_prec_bits > 0) {
+    if (lane == 0) round_to_prec(out, W, round_prec_bits, ovf);
+    ovf = __shfl_sync(full, ovf, 0);
+    __syncwarp();
+  }
+  int bot = 1 << 30, tp = -1;
+  for (int d = lane; d < W; d += 32)
+    if (out[d]) {
+      bot = min(bot, d);
+      tp = max(tp, d);
+    }
+  bot = __reduce_min_sync(full, bot);
+  tp = __reduce_max_sync(full, tp);
+  if (lane == 0) *info = make_int2(tp >= 0 ? bot : W, tp);
+  __syncwarp();
+  return ovf;
+}
+
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void copy_row(int32_t* dst, const int32_t* __restrict__ src, int RS) {
+  for (int d = threadIdx.x; d < RS; d += blockDim.x) dst[d] = src[d];
+}
+
+template <int NPT>
+__global__ void __launch_bounds__(256, 1) taylor_team_kernel(const __grid_constant__ Params p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const Geo g = make_geo(p);
+  const Layout L = make_layout(p);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int warp = tid >> 5, nwarps = nt >> 5;
+  const int traj = blockIdx.x;
+  if (traj >= p.n_traj) return;
+
+  int32_t* stage = (int32_t*)(smem + L.off_stage);
+  int2* stinfo = (int2*)(smem + L.off_sinfo);
+  int32_t* crow = (int32_t*)(smem + L.off_const);
+  int2* cinfo = (int2*)(smem + L.off_cinfo);
+  int32_t* cur = (int32_t*)(smem + L.off_cur);
+  int2* curinfo = (int2*)(smem + L.off_curinfo);
+  int32_t* srow = (int32_t*)(smem + L.off_s);
+  int2* sinf = (int2*)(smem + L.off_sinf);
+  int32_t* urow = (int32_t*)(smem + L.off_u);
+  int2* uinf = (int2*)(smem + L.off_uinf);
+  int32_t* ctrow = (int32_t*)(smem + L.off_ct);
+  int2* ctinf = (int2*)(smem + L.off_ctinf);
+  int64_t* part = (int64_t*)(smem + L.off_part);
+  int64_t* colsum = (int64_t*)(smem + L.off_col);
+  int* uout = (int*)(smem + L.off_uout);
+  int* flag = (int*)(smem + L.off_flag);
+  const int rw = L.rw;
+  auto ROW = [&](int32_t* base, int r) { return base + (size_t)r * rw + kPad; };
+
+  // zero all of shared memory once (pads stay zero forever)
+  for (size_t w = tid; w < L.total / 4; w += nt) ((int32_t*)smem)[w] = 0;
+  if (tid == 0) flag[0] = 0;
+  __syncthreads();
+
+  // constant rows: cst (D), lin (D*D), q (NT)
+  for (int r = 0; r < L.n_const_rows; r++) {
+    const int32_t* src = r < p.D ? p.cst + (size_t)r * p.RS
+                         : r < p.D + p.D * p.D ? p.lin + (size_t)(r - p.D) * p.RS
+                                                : p.q + (size_t)(r - p.D - p.D * p.D) * p.RS;
+    copy_row(ROW(crow, r), src, p.RS);
+  }
+  __syncthreads();
+  for (int r = warp; r < L.n_const_rows; r += nwarps) {
+    int bot = 1 << 30, tp = -1;
+    const int32_t* row = ROW(crow, r);
+    for (int d = (tid & 31); d < p.W; d += 32)
+      if (row[d]) {
+        bot = min(bot, d);
+        tp = max(tp, d);
+      }
+    bot = __reduce_min_sync(0xffffffffu, bot);
+    tp = __reduce_max_sync(0xffffffffu, tp);
+    if ((tid & 31) == 0) cinfo[r] = make_int2(tp >= 0 ? bot : p.W, tp);
+  }
+
+  const size_t traj_rows = (size_t)p.D * (p.N + 1);
+  int32_t* gcoef = p.coef + (size_t)traj * traj_rows * p.RS;
+  int2* ginfo = p.rinfo + (size_t)traj * traj_rows;
+  int32_t* gstate = p.state + (size_t)traj * p.D * p.RS;
+  auto GROW = [&](int m, int i) { return gcoef + ((size_t)m * (p.N + 1) + i) * p.RS; };
+  auto GINF = [&](int m, int i) -> int2& { return ginfo[(size_t)m * (p.N + 1) + i]; };
+
+  // initial state -> cur rows (normalised info computed from digits)
+  for (int m = 0; m < p.D; m++) copy_row(ROW(cur, m), gstate + (size_t)m * p.RS, p.RS);
+  __syncthreads();
+
+  const int ns_a = max(1, nt / g.NGb);  // k slots in phase A
+  int status = 0;
+
+  for (int n = p.start_step + 1; n <= p.n_steps; n++) {
+    // coefficient row 0 = state
+    for (int m = warp; m < p.D; m += nwarps) {
+      int bot = 1 << 30, tp = -1;
+      const int32_t* row = ROW(cur, m);
+      for (int d = (tid & 31); d < p.W; d += 32)
+        if (row[d]) {
+          bot = min(bot, d);
+          tp = max(tp, d);
+        }
+      bot = __reduce_min_sync(0xffffffffu, bot);
+      tp = __reduce_max_sync(0xffffffffu, tp);
+      if ((tid & 31) == 0) {
+        curinfo[m] = make_int2(tp >= 0 ? bot : p.W, tp);
+        GINF(m, 0) = curinfo[m];
+      }
+    }
+    for (int m = 0; m < p.D; m++)
+      for (int d = tid; d < p.RS; d += nt) GROW(m, 0)[d] = ROW(cur, m)[d];
+    __syncthreads();
+
+    for (int i = 0; i < p.N; i++) {
+      // ===================== phase A: Cauchy sums =====================
+      if (p.NP > 0) {
+        const int slot = tid / g.NGb, grp = tid % g.NGb;
+        const bool active = slot < ns_a;
+        const int c0 = kR * (g.gfb + grp);
+        Acc acc[NPT];
+#pragma unroll
+        for (int q = 0; q < NPT; q++) acc_zero(acc[q]);
+        int cnt = 0;
+        const int nrows = p.nlv + p.nrv;
+        for (int k0 = 0; k0 <= i; k0 += p.kc) {
+          const int kcn = min(p.kc, i + 1 - k0);
+          // stage rows
+          for (int kk = 0; kk < kcn; kk++) {
+            const int k = k0 + kk;
+            for (int v = 0; v < nrows; v++) {
+              const int32_t* src = v < p.nlv ? GROW(p.lvar[v], i - k) : GROW(p.rvar[v - p.nlv], k);
+              copy_row(ROW(stage, kk * nrows + v), src, p.RS);
+              if (tid == 0)
+                stinfo[kk * nrows + v] = v < p.nlv ? GINF(p.lvar[v], i - k) : GINF(p.rvar[v - p.nlv], k);
+            }
+          }
+          __syncthreads();
+          if (active) {
+            for (int kk = slot; kk < kcn; kk += ns_a) {
+#pragma unroll
+              for (int q = 0; q < NPT; q++) {
+                if (q < p.NP) {
+                  const int ra = kk * nrows + p.pl[q];
+                  const int rb = kk * nrows + p.nlv + p.pr[q];
+                  mac_group(acc[q], cnt, ROW(stage, ra), stinfo[ra], ROW(stage, rb), stinfo[rb], c0, g.Tb);
+                }
+              }
+            }
+          }
+          __syncthreads();
+        }
+        // partials: unit = slot * NP + q, columns relative to Tb
+        if (active) {
+#pragma unroll
+          for (int q = 0; q < NPT; q++) {
+            if (q < p.NP) {
+              acc_fold(acc[q], c0, g.Tb);
+              int64_t* pr = part + (size_t)(slot * p.NP + q) * g.NCX;
+#pragma unroll
+              for (int r = 0; r < kR; r++) {
+                int c = c0 + r - g.Tb;
+                if (c >= 0) pr[c] = acc[q].v[r];
+              }
+            }
+          }
+        }
+        for (int u = tid; u < ns_a * p.NP; u += nt) uout[u] = u % p.NP;
+        __syncthreads();
+        if (active) {
+#pragma unroll
+          for (int q = 0; q < NPT; q++) {
+            if (q < p.NP) {
+              int c = c0 + kR - g.Tb;
+              part[(size_t)(slot * p.NP + q) * g.NCX + c] += acc[q].v[kR];
+            }
+          }
+        }
+        __syncthreads();
+        // reduce units -> colsum[q][c]
+        const int ncol = kR * (g.gfb + g.NGb) - g.Tb + 1;
+        for (int e = tid; e < p.NP * ncol; e += nt) {
+          int q = e / ncol, c = e % ncol;
+          int64_t s = 0;
+          for (int sl = 0; sl < ns_a; sl++) s += part[(size_t)(sl * p.NP + q) * g.NCX + c];
+          colsum[(size_t)q * g.NCX + c] = s;
+        }
+        // clear partials for the next use
+        __syncthreads();
+        for (size_t w = tid; w < (size_t)ns_a * p.NP * g.NCX; w += nt) part[w] = 0;
+        for (int q = warp; q < p.NP; q += nwarps) {
+          bool o = warp_normalize(colsum + (size_t)q * g.NCX, ncol, 2, p.W, ROW(srow, q), &sinf[q], 0);
+          if (o && (tid & 31) == 0) flag[0] = 1;
+        }
+        __syncthreads();
+      }
+      // ===================== phase B: numerators =====================
+      {
+        // items: lin (m, j) for nonzero L_mj, then bilinear terms
+        const int nlin = p.D * p.D;
+        const int nitems = nlin + p.NT;
+        for (int u = tid; u < nitems; u += nt) uout[u] = u < nlin ? u / p.D : p.teq[u - nlin];
+        // every thread: (item, grp)
+        for (int e = tid; e < nitems * g.NGb; e += nt) {
+          const int it = e / g.NGb, grp = e % g.NGb;
+          const int c0 = kR * (g.gfb + grp);
+          const int32_t *A, *B;
+          int2 ia, ib;
+          if (it < nlin) {
+            const int m = it / p.D, j = it % p.D;
+            A = ROW(crow, p.D + m * p.D + j);
+            ia = cinfo[p.D + m * p.D + j];
+            B = ROW(cur, j);
+            ib = curinfo[j];
+          } else {
+            const int t = it - nlin;
+            A = ROW(crow, p.D + nlin + t);
+            ia = cinfo[p.D + nlin + t];
+            B = ROW(srow, p.tpair[t]);
+            ib = sinf[p.tpair[t]];
+          }
+          Acc acc;
+          acc_zero(acc);
+          int cnt = 0;
+          mac_group(acc, cnt, A, ia, B, ib, c0, g.Tb);
+          acc_fold(acc, c0, g.Tb);
+          int64_t* pr = part + (size_t)it * g.NCX;
+#pragma unroll
+          for (int r = 0; r <= kR; r++) {
+            int c = c0 + r - g.Tb;
+            if (c >= 0) atomicAdd((unsigned long long*)&pr[c], (unsigned long long)acc.v[r]);
+          }
+        }
+        __syncthreads();
+        const int ncol = kR * (g.gfb + g.NGb) - g.Tb + 1;
+        for (int e = tid; e < p.D * ncol; e += nt) {
+          int m = e / ncol, c = e % ncol;
+          int64_t s = 0;
+          for (int u = 0; u < nitems; u++)
+            if (uout[u] == m) s += part[(size_t)u * g.NCX + c];
+          if (i == 0 && c >= 2 && c - 2 < p.W) s += ROW(crow, m)[c - 2];
+          colsum[(size_t)m * g.NCX + c] = s;
+        }
+        __syncthreads();
+        for (size_t w = tid; w < (size_t)nitems * g.NCX; w += nt) part[w] = 0;
+        // tau/(i+1) row for phase C
+        copy_row(ROW(ctrow, 0), p.ctab + (size_t)i * p.RS, p.RS);
+        for (int m = warp; m < p.D; m += nwarps) {
+          bool o = warp_normalize(colsum + (size_t)m * g.NCX, ncol, 2, p.W, ROW(urow, m), &uinf[m], 0);
+          if (o && (tid & 31) == 0) flag[0] = 1;
+        }
+        __syncthreads();
+        if (warp == 0) {
+          int bot = 1 << 30, tp = -1;
+          const int32_t* row = ROW(ctrow, 0);
+          for (int d = (tid & 31); d < p.W; d += 32)
+            if (row[d]) {
+              bot = min(bot, d);
+              tp = max(tp, d);
+            }
+          bot = __reduce_min_sync(0xffffffffu, bot);
+          tp = __reduce_max_sync(0xffffffffu, tp);
+          if (tid == 0) ctinf[0] = make_int2(tp >= 0 ? bot : p.W, tp);
+        }
+        __syncthreads();
+      }
+      // ===================== phase C: scale by tau/(i+1) =====================
+      {
+        for (int e = tid; e < p.D * g.NGc; e += nt) {
+          const int m = e / g.NGc, grp = e % g.NGc;
+          const int c0 = kR * (g.gfc + grp);
+          Acc acc;
+          acc_zero(acc);
+          int cnt = 0;
+          mac_group(acc, cnt, ROW(urow, m), uinf[m], ROW(ctrow, 0), ctinf[0], c0, g.Tc);
+          acc_fold(acc, c0, g.Tc);
+          int64_t* pr = part + (size_t)m * g.NCX;
+#pragma unroll
+          for (int r = 0; r <= kR; r++) {
+            int c = c0 + r - g.Tc;
+            if (c >= 0) atomicAdd((unsigned long long*)&pr[c], (unsigned long long)acc.v[r]);
+          }
+        }
+        __syncthreads();
+        const int ncol = kR * (g.gfc + g.NGc) - g.Tc + 1;
+        for (int m = warp; m < p.D; m += nwarps) {
+          bool o = warp_normalize(part + (size_t)m * g.NCX, ncol, 2, p.W, ROW(cur, m), &curinfo[m], 0);
+          if (o && (tid & 31) == 0) flag[0] = 1;
+        }
+        __syncthreads();
+        for (size_t w = tid; w < (size_t)p.D * g.NCX; w += nt) part[w] = 0;
+        for (int m = 0; m < p.D; m++)
+          for (int d = tid; d < p.RS; d += nt) GROW(m, i + 1)[d] = ROW(cur, m)[d];
+        if (tid < p.D) GINF(tid, i + 1) = curinfo[tid];
+        __syncthreads();
+      }
+    }
+    // ===================== state update: exact sum of rows, round to P bits ===========
+    {
+      const int ncol = p.W + 3;
+      for (int e = tid; e < p.D * ncol; e += nt) {
+        int m = e / ncol, c = e % ncol;
+        int64_t s = 0;
+        if (c < p.W)
+          for (int i = 0; i <= p.N; i++) s += GROW(m, i)[c];
+        colsum[(size_t)m * g.NCX + c] = s;
+      }
+      __syncthreads();
+      for (int m = warp; m < p.D; m += nwarps) {
+        bool o = warp_normalize(colsum + (size_t)m * g.NCX, ncol, 0, p.W, ROW(cur, m), &curinfo[m], p.P);
+        if (o && (tid & 31) == 0) flag[0] = 1;
+      }
+      __syncthreads();
+      // record
+      const bool rec = (n % p.stride == 0) || (n == p.n_steps);
+      if (rec) {
+        int slot = (n % p.stride == 0) ? (n / p.stride - p.start_step / p.stride)
+                                       : (p.n_steps / p.stride - p.start_step / p.stride + 1);
+        int32_t* dst = p.rec + ((size_t)slot * p.n_traj + traj) * p.D * p.RS;
+        for (int m = 0; m < p.D; m++)
+          for (int d = tid; d < p.RS; d += nt) dst[(size_t)m * p.RS + d] = ROW(cur, m)[d];
+      }
+      __syncthreads();
+    }
+  }
+  for (int m = 0; m < p.D; m++)
+    for (int d = tid; d < p.RS; d += nt) gstate[(size_t)m * p.RS + d] = ROW(cur, m)[d];
+  if (tid == 0) {
+    status = flag[0] ? kOverflow : kOk;
+    p.status[traj] = status;
+  }
+}
+
+cudaError_t launch_team_kernel(const Params& p, size_t smem, cudaStream_t stream) {
+  const int npt = p.NP <= 1 ? 1 : p.NP <= 2 ? 2 : p.NP <= 4 ? 4 : 8;
+  const void* fn = npt == 1   ? (const void*)taylor_team_kernel<1>
+                   : npt == 2 ? (const void*)taylor_team_kernel<2>
+                   : npt == 4 ? (const void*)taylor_team_kernel<4>
+                              : (const void*)taylor_team_kernel<8>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  Params pc = p;
+  void* args[] = {&pc};
+  return cudaLaunchKernel(fn, dim3(p.n_traj), dim3(p.nthreads), args, smem, stream);
+}
+
+size_t smem_bytes(const Params& p) { return make_layout(p).total; }
+
+}  // namespace mpt
