@@ -104,6 +104,16 @@ float mpt_last_kernel_ms(const mpt_plan *plan);
 /* dynamic shared memory per CTA and k-chunk chosen for this plan */
 int mpt_plan_info(const mpt_plan *plan, int *smem_bytes, int *k_chunk, int *threads);
 
+/* ---- measurement helpers (bench.py roofline; not part of the reference interface) ---- */
+/* count limb-MACs in subsequent launches: useful = digit products inside the
+   nonzero windows (algorithmic work), executed = issued IMAD.WIDE lanes */
+int mpt_count_macs(mpt_plan *plan, int enable);
+int mpt_read_macs(mpt_plan *plan, unsigned long long *useful, unsigned long long *executed);
+/* measured IMAD.WIDE (s64 += s32*s32) throughput of the whole device, per second */
+int mpt_imad_probe(int device, double *imad_per_second, float *ms);
+/* write `bytes` of a scratch buffer (L2 flush between timed launches) */
+int mpt_l2_flush(int device, size_t bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -32,6 +32,10 @@ EXPORTS = (
     "mpt_step",
     "mpt_last_kernel_ms",
     "mpt_plan_info",
+    "mpt_count_macs",
+    "mpt_read_macs",
+    "mpt_imad_probe",
+    "mpt_l2_flush",
 )
 
 
@@ -71,6 +75,11 @@ def _declare(L):
     L.mpt_last_kernel_ms.argtypes = [vp]
     L.mpt_last_kernel_ms.restype = ctypes.c_float
     L.mpt_plan_info.argtypes = [vp, i32p, i32p, i32p]
+    u64p = ctypes.POINTER(ctypes.c_ulonglong)
+    L.mpt_count_macs.argtypes = [vp, ctypes.c_int]
+    L.mpt_read_macs.argtypes = [vp, u64p, u64p]
+    L.mpt_imad_probe.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_float)]
+    L.mpt_l2_flush.argtypes = [ctypes.c_int, ctypes.c_size_t]
 
 
 def load(require_device: bool = True):

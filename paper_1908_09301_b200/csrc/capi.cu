@@ -13,6 +13,7 @@
 namespace mpt {
 size_t smem_bytes(const Params& p);
 cudaError_t launch_team_kernel(const Params& p, size_t smem, cudaStream_t stream);
+cudaError_t launch_imad_probe(int blocks, int threads, int iters, long long* out, cudaStream_t s);
 }  // namespace mpt
 
 static thread_local std::string g_err;
@@ -41,6 +42,8 @@ struct mpt_plan {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   float last_ms = 0.f;
   bool have_constants = false;
+  unsigned long long* d_counters = nullptr;
+  bool counting = false;
 };
 
 extern "C" {
@@ -193,6 +196,7 @@ int mpt_plan_destroy(mpt_plan* pl) {
   cudaFree(pl->d_state);
   cudaFree(pl->d_rec);
   cudaFree(pl->d_status);
+  cudaFree(pl->d_counters);
   if (pl->ev0) cudaEventDestroy(pl->ev0);
   if (pl->ev1) cudaEventDestroy(pl->ev1);
   delete pl;
@@ -253,6 +257,7 @@ static int launch(mpt_plan* pl, int n_steps, int start_step, int stride, cudaStr
   p.start_step = start_step;
   p.stride = stride;
   p.rec = pl->d_rec;
+  p.counters = pl->counting ? pl->d_counters : nullptr;
   CK(cudaEventRecord(pl->ev0, stream));
   CK(mpt::launch_team_kernel(p, pl->smem, stream));
   CK(cudaEventRecord(pl->ev1, stream));
@@ -352,6 +357,74 @@ int mpt_step(mpt_plan* pl, const int32_t* state, int32_t* state_out, int32_t* st
   return MPT_OK;
 }
 
-float mpt_last_kernel_ms(const mpt_plan* pl) { return pl ? pl->last_ms : -1.f; }
+float mpt_last_kernel_ms(const mpt_plan* pl) {
+  if (!pl) return -1.f;
+  // the launch may have been asynchronous (mpt_integrate_device): wait for its end event
+  if (cudaEventSynchronize(pl->ev1) == cudaSuccess) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, pl->ev0, pl->ev1) == cudaSuccess) return ms;
+  }
+  cudaGetLastError();
+  return pl->last_ms;
+}
+
+int mpt_count_macs(mpt_plan* pl, int enable) {
+  if (!pl) return fail(MPT_EINVAL, "null plan");
+  CK(cudaSetDevice(pl->device));
+  if (enable && !pl->d_counters) CK(cudaMalloc((void**)&pl->d_counters, 2 * sizeof(unsigned long long)));
+  if (pl->d_counters) CK(cudaMemset(pl->d_counters, 0, 2 * sizeof(unsigned long long)));
+  pl->counting = enable != 0;
+  return MPT_OK;
+}
+
+int mpt_read_macs(mpt_plan* pl, unsigned long long* useful, unsigned long long* executed) {
+  if (!pl || !pl->d_counters) return fail(MPT_EINVAL, "counting not enabled");
+  unsigned long long h[2];
+  CK(cudaMemcpy(h, pl->d_counters, sizeof h, cudaMemcpyDeviceToHost));
+  if (useful) *useful = h[0];
+  if (executed) *executed = h[1];
+  return MPT_OK;
+}
+
+int mpt_imad_probe(int device, double* per_second, float* ms_out) {
+  if (mpt_device_count() <= 0) return fail(MPT_ENODEV, "no CUDA device available");
+  CK(cudaSetDevice(device));
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  long long* out = nullptr;
+  CK(cudaMalloc((void**)&out, sizeof(long long)));
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int threads = 512, blocks = sms * 4, iters = 4096;
+  CK(mpt::launch_imad_probe(blocks, threads, 64, out, 0));  // warm-up
+  CK(cudaEventRecord(a, 0));
+  CK(mpt::launch_imad_probe(blocks, threads, iters, out, 0));
+  CK(cudaEventRecord(b, 0));
+  CK(cudaEventSynchronize(b));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(out);
+  double ops = (double)blocks * threads * iters * 64.0;  // 8 unrolled x 8 chains
+  if (per_second) *per_second = ops / (ms * 1e-3);
+  if (ms_out) *ms_out = ms;
+  return MPT_OK;
+}
+
+int mpt_l2_flush(int device, size_t bytes) {
+  static void* buf = nullptr;
+  static size_t have = 0;
+  CK(cudaSetDevice(device));
+  if (bytes > have) {
+    cudaFree(buf);
+    buf = nullptr;
+    CK(cudaMalloc(&buf, bytes));
+    have = bytes;
+  }
+  CK(cudaMemsetAsync(buf, have & 1, bytes, 0));
+  return MPT_OK;
+}
 
 }  // extern "C"

@@ -51,6 +51,7 @@ struct Params {
   int n_steps, start_step, stride;
   int kc;               // k values staged per chunk
   int nthreads;
+  unsigned long long* counters;  // optional: [0] useful limb-MACs, [1] executed limb-MACs
 };
 
 }  // namespace mpt

@@ -125,13 +125,35 @@ __device__ __forceinline__ void acc_fold(Acc& a, int c0, int tcut) {
   }
 }
 
+struct MacCount {
+  unsigned long long useful = 0, executed = 0;
+};
+
+// exact number of digit products (p, q) inside the nonzero windows that fall
+// in the group's kept columns [max(c0, tcut), c0 + kR) -- the algorithmic work
+__device__ __forceinline__ unsigned useful_macs(int2 ia, int2 ib, int c0, int tcut) {
+  unsigned n = 0;
+#pragma unroll
+  for (int r = 0; r < kR; r++) {
+    int c = c0 + r;
+    int lo = max(ia.x, c - ib.y), hi = min(ia.y, c - ib.x);
+    if (c >= tcut && hi >= lo) n += hi - lo + 1;
+  }
+  return n;
+}
+
 __device__ __forceinline__ void mac_group(Acc& acc, int& cnt, const int32_t* __restrict__ A, int2 ia,
-                                          const int32_t* __restrict__ B, int2 ib, int c0, int tcut) {
+                                          const int32_t* __restrict__ B, int2 ib, int c0, int tcut,
+                                          MacCount* mc = nullptr) {
   // nonzero digits: A in [ia.x, ia.y], B in [ib.x, ib.y]
   int plo = max(ia.x, c0 - ib.y);
   int phi = min(ia.y, c0 + kR - 1 - ib.x);
   if (plo > phi) return;
   int P0 = plo & ~(kR - 1);
+  if (mc) {
+    mc->useful += useful_macs(ia, ib, c0, tcut);
+    mc->executed += (unsigned long long)(((phi - P0) / kR + 1) * kR * kR);
+  }
   int32_t buf[kR];
   const int32_t* bq = B + (c0 - P0);  // bq[s] = B[c0 - P0 + s]
 #pragma unroll
@@ -369,6 +391,8 @@ __global__ void __launch_bounds__(256, 1) taylor_team_kernel(const __grid_consta
 
   const int ns_a = max(1, nt / g.NGb);  // k slots in phase A
   int status = 0;
+  MacCount mcount;
+  MacCount* mc = p.counters ? &mcount : nullptr;
 
   for (int n = p.start_step + 1; n <= p.n_steps; n++) {
     // coefficient row 0 = state
@@ -404,14 +428,21 @@ __global__ void __launch_bounds__(256, 1) taylor_team_kernel(const __grid_consta
         const int nrows = p.nlv + p.nrv;
         for (int k0 = 0; k0 <= i; k0 += p.kc) {
           const int kcn = min(p.kc, i + 1 - k0);
-          // stage rows
-          for (int kk = 0; kk < kcn; kk++) {
-            const int k = k0 + kk;
-            for (int v = 0; v < nrows; v++) {
+          // stage rows: one flat, 16-byte vectorised copy of all kcn*nrows rows
+          {
+            const int q4 = p.RS / 4;
+            const int total = kcn * nrows * q4;
+            for (int e = tid; e < total; e += nt) {
+              const int r = e / q4, w = e - r * q4;
+              const int kk = r / nrows, v = r - kk * nrows;
+              const int k = k0 + kk;
               const int32_t* src = v < p.nlv ? GROW(p.lvar[v], i - k) : GROW(p.rvar[v - p.nlv], k);
-              copy_row(ROW(stage, kk * nrows + v), src, p.RS);
-              if (tid == 0)
-                stinfo[kk * nrows + v] = v < p.nlv ? GINF(p.lvar[v], i - k) : GINF(p.rvar[v - p.nlv], k);
+              reinterpret_cast<int4*>(ROW(stage, r))[w] = __ldcg(reinterpret_cast<const int4*>(src) + w);
+            }
+            for (int r = tid; r < kcn * nrows; r += nt) {
+              const int kk = r / nrows, v = r - kk * nrows;
+              const int k = k0 + kk;
+              stinfo[r] = v < p.nlv ? GINF(p.lvar[v], i - k) : GINF(p.rvar[v - p.nlv], k);
             }
           }
           __syncthreads();
@@ -422,7 +453,7 @@ __global__ void __launch_bounds__(256, 1) taylor_team_kernel(const __grid_consta
                 if (q < p.NP) {
                   const int ra = kk * nrows + p.pl[q];
                   const int rb = kk * nrows + p.nlv + p.pr[q];
-                  mac_group(acc[q], cnt, ROW(stage, ra), stinfo[ra], ROW(stage, rb), stinfo[rb], c0, g.Tb);
+                  mac_group(acc[q], cnt, ROW(stage, ra), stinfo[ra], ROW(stage, rb), stinfo[rb], c0, g.Tb, mc);
                 }
               }
             }
@@ -501,7 +532,7 @@ __global__ void __launch_bounds__(256, 1) taylor_team_kernel(const __grid_consta
           Acc acc;
           acc_zero(acc);
           int cnt = 0;
-          mac_group(acc, cnt, A, ia, B, ib, c0, g.Tb);
+          mac_group(acc, cnt, A, ia, B, ib, c0, g.Tb, mc);
           acc_fold(acc, c0, g.Tb);
           int64_t* pr = part + (size_t)it * g.NCX;
 #pragma unroll
@@ -551,7 +582,7 @@ __global__ void __launch_bounds__(256, 1) taylor_team_kernel(const __grid_consta
           Acc acc;
           acc_zero(acc);
           int cnt = 0;
-          mac_group(acc, cnt, ROW(urow, m), uinf[m], ROW(ctrow, 0), ctinf[0], c0, g.Tc);
+          mac_group(acc, cnt, ROW(urow, m), uinf[m], ROW(ctrow, 0), ctinf[0], c0, g.Tc, mc);
           acc_fold(acc, c0, g.Tc);
           int64_t* pr = part + (size_t)m * g.NCX;
 #pragma unroll
@@ -608,6 +639,38 @@ __global__ void __launch_bounds__(256, 1) taylor_team_kernel(const __grid_consta
     status = flag[0] ? kOverflow : kOk;
     p.status[traj] = status;
   }
+  if (mc) {
+    atomicAdd(&p.counters[0], mcount.useful);
+    atomicAdd(&p.counters[1], mcount.executed);
+  }
+}
+
+// Integer-pipe roofline probe: every thread runs 8 independent IMAD.WIDE
+// chains (s64 += s32 * s32) -- the instruction the Cauchy loop is built on.
+__global__ void imad_wide_probe(int iters, int32_t seed, long long* out) {
+  int64_t a0 = seed, a1 = seed + 1, a2 = seed + 2, a3 = seed + 3, a4 = seed + 4, a5 = seed + 5,
+          a6 = seed + 6, a7 = seed + 7;
+  int32_t x = threadIdx.x | 1, y = blockIdx.x | 3;
+  for (int i = 0; i < iters; i++) {
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+      a0 += (int64_t)x * y;
+      a1 += (int64_t)(x + 1) * y;
+      a2 += (int64_t)(x + 2) * y;
+      a3 += (int64_t)(x + 3) * y;
+      a4 += (int64_t)(x + 4) * y;
+      a5 += (int64_t)(x + 5) * y;
+      a6 += (int64_t)(x + 6) * y;
+      a7 += (int64_t)(x + 7) * y;
+      y ^= (int32_t)(a0 >> 40);
+    }
+  }
+  if ((a0 ^ a1 ^ a2 ^ a3 ^ a4 ^ a5 ^ a6 ^ a7) == 0x123456789LL) out[0] = a0;
+}
+
+cudaError_t launch_imad_probe(int blocks, int threads, int iters, long long* out, cudaStream_t s) {
+  imad_wide_probe<<<blocks, threads, 0, s>>>(iters, 7, out);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_team_kernel(const Params& p, size_t smem, cudaStream_t stream) {

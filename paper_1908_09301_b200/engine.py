@@ -152,3 +152,11 @@ class DevicePlan:
 
     def last_kernel_ms(self) -> float:
         return float(self.lib.mpt_last_kernel_ms(self.h))
+
+    def count_macs(self, enable: bool = True):
+        _native.check(self.lib.mpt_count_macs(self.h, 1 if enable else 0))
+
+    def read_macs(self):
+        u, x = ctypes.c_ulonglong(), ctypes.c_ulonglong()
+        _native.check(self.lib.mpt_read_macs(self.h, ctypes.byref(u), ctypes.byref(x)))
+        return u.value, x.value

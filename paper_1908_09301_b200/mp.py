@@ -255,10 +255,12 @@ def mp_from_decimal(text: str, ctx: PrecisionContext) -> MPValue:
     whole, _, frac = mant_txt.partition(".")
     digits = int((whole or "0") + frac) if (whole or frac) else 0
     e10 -= len(frac)
-    if abs(e10) > 2 * 10**9:
-        raise RangeError(f"decimal exponent out of range: {text!r}")
     if digits == 0:
         return MPValue(-1 if neg else 1, 0, 0, ctx.precision_bits)
+    # decimal magnitude ~ 10^(len(digits) + e10): reject before building huge powers
+    approx_bits = (len(str(digits)) + e10) * 3.3219280948873626
+    if approx_bits > _EMAX + 8 or approx_bits < _EMIN - 8:
+        raise RangeError(f"decimal exponent out of range: {text!r}")
     f = Fraction(digits) * (Fraction(10) ** e10)
     if neg:
         f = -f

@@ -1,0 +1,220 @@
+"""GPU parity tests (B200): the CUDA path through the C ABI against
+  (1) the bit-exact model of the device arithmetic (oracle/fixmodel.c), and
+  (2) the reference's frozen outputs (tests/golden, pinned to the unmodified
+      reference) within relative 10^-(K-d), d = 3 + ceil(0.3935 t).
+Edge cases follow the reference's tests: zero state, zero steps, backward
+step, single-dimension system, random quadratic systems, resume, observer,
+determinism."""
+
+import math
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import paper_1908_09301_b200 as M
+from oracle import fix as FX
+from paper_1908_09301_b200.engine import DevicePlan, SystemTables
+from paper_1908_09301_b200.fixed import FixedFormat
+
+from .conftest import CANON_INIT
+from .helpers import EXACT, agreement_digits, frac, system_from_json
+
+pytestmark = pytest.mark.gpu
+
+
+def guard_digits(t: float) -> int:
+    return 3 + math.ceil(0.3935 * t)
+
+
+def lorenz_tables(P, N, tau="0.01", guard=32, scale=None):
+    ctx = M.PrecisionContext(P)
+    system = M.builtin_system("lorenz", ctx)
+    fmt = FixedFormat(P, guard)
+    s = scale if scale is not None else M.mp_from_decimal(tau, ctx).as_fraction()
+    return ctx, system, fmt, SystemTables.build(system, fmt, N, s)
+
+
+# ---------------------------------------------------------------- bit-exact
+@pytest.mark.parametrize("P,N,steps,stride", [(128, 20, 30, 10), (167, 40, 40, 10), (256, 30, 25, 5),
+                                               (1661, 200, 3, 1), (2658, 240, 2, 1)])
+def test_integrate_bit_exact_vs_model(gpu, P, N, steps, stride):
+    ctx, system, fmt, tables = lorenz_tables(P, N)
+    st = fmt.to_digits([M.mp_from_decimal(t, ctx) for t in CANON_INIT])
+    with DevicePlan(tables, fmt, N, 1) as plan:
+        s_gpu, r_gpu, status = plan.integrate(st, steps, 0, stride)
+    s_cpu, r_cpu = FX.integrate(tables, fmt.frac_digits, N, P, st, steps, 0, stride)
+    assert status.tolist() == [0]
+    assert list(s_gpu) == list(s_cpu)
+    assert np.array_equal(r_gpu[:, 0], r_cpu)
+
+
+def test_jet_bit_exact_vs_model_large_order(gpu):
+    P, N = 1661, 200
+    ctx, system, fmt, tables = lorenz_tables(P, N)
+    st = fmt.to_digits([M.mp_from_decimal(t, ctx) for t in CANON_INIT])
+    with DevicePlan(tables, fmt, N, 1) as plan:
+        g = plan.compute_jet(st)[0]
+    c = FX.compute_jet(tables, fmt.frac_digits, N, st)
+    assert np.array_equal(g, c)
+
+
+def test_ensemble_of_trajectories_bit_exact(gpu):
+    P, N, n_traj = 256, 30, 5
+    ctx, system, fmt, tables = lorenz_tables(P, N)
+    base = [M.mp_from_decimal(t, ctx).as_fraction() for t in CANON_INIT]
+    states = np.stack([fmt.to_digits([b + Fraction(j, 10**20) for b in base]) for j in range(n_traj)])
+    with DevicePlan(tables, fmt, N, n_traj) as plan:
+        _, r_gpu, status = plan.integrate(states, 12, 0, 4)
+    assert not status.any()
+    for j in range(n_traj):
+        _, r_cpu = FX.integrate(tables, fmt.frac_digits, N, P, states[j], 12, 0, 4)
+        assert np.array_equal(r_gpu[:, j], r_cpu), j
+
+
+def test_random_quadratic_systems_jets_bit_exact(golden, gpu):
+    for name, c in golden.items():
+        if not name.startswith("random_jet"):
+            continue
+        P, N = c["prec_bits"], c["order"]
+        ctx = M.PrecisionContext(P)
+        system = system_from_json(c["system"], ctx)
+        fmt = FixedFormat(P)
+        tables = SystemTables.build(system, fmt, N, Fraction(1, 128))
+        st = fmt.to_digits([frac(h) for h in c["state"]])
+        with DevicePlan(tables, fmt, N, 1) as plan:
+            g = plan.compute_jet(st)[0]
+        assert np.array_equal(g, FX.compute_jet(tables, fmt.frac_digits, N, st)), name
+
+
+# ---------------------------------------------------- parity vs reference
+@pytest.mark.parametrize("name", ["config0_k50_n40", "cns_pair_128_n20", "cns_pair_256_n30",
+                                  "config1_k500_n200_3steps", "backward_256_n30", "zero_state_256_n8"])
+def test_dropin_integrate_matches_reference(golden, gpu, name):
+    c = golden[name]
+    P = c["prec_bits"]
+    ctx = M.PrecisionContext(P)
+    system = M.builtin_system("lorenz", ctx)
+    state0 = tuple(M.mp_from_decimal(t, ctx) for t in c["init"])
+    traj = M.integrate(system, state0, M.StepConfig(c["tau"], c["order"]), c["n_steps"], ctx,
+                       record_stride=c["stride"])
+    assert traj.steps() == [r["step"] for r in c["records"]]
+    K = M.decimal_digits(P)
+    tau = abs(float(Fraction(c["tau"])))
+    for pt, rec in zip(traj.points, c["records"]):
+        assert all(v.precision == P for v in pt.state)
+        got = [v.as_fraction() for v in pt.state]
+        ref = [frac(h) for h in rec["state"]]
+        d = agreement_digits(got, ref)
+        assert d == EXACT or d >= K - guard_digits(pt.step * tau), (name, pt.step, d)
+
+
+def test_reference_regression_pair_on_gpu(gpu):
+    """The reference's frozen agreement series (tests/test_cns.py:105), from GPU runs."""
+    runs = {}
+    for P, N in ((128, 20), (256, 30)):
+        ctx = M.PrecisionContext(P)
+        system = M.builtin_system("lorenz", ctx)
+        state0 = tuple(M.mp_from_decimal(t, ctx) for t in CANON_INIT)
+        runs[P] = M.integrate(system, state0, M.StepConfig("0.01", N), 2500, ctx, record_stride=100)
+    series = {a.step: agreement_digits([v.as_fraction() for v in a.state], [v.as_fraction() for v in b.state])
+              for a, b in zip(runs[128].points, runs[256].points)}
+    assert series[0] == 38
+    assert 22 <= series[100] <= 24  # reference: 23
+    assert 12 <= series[2500] <= 14  # reference: 13
+    assert min(series.values()) >= 6  # t_c = 25 at d = 6, as in the reference
+
+
+# -------------------------------------------------------- drop-in behaviour
+def _lorenz(P=256):
+    ctx = M.PrecisionContext(P)
+    return ctx, M.builtin_system("lorenz", ctx), tuple(M.mp_from_decimal(t, ctx) for t in CANON_INIT)
+
+
+def test_recording_policy_and_zero_steps(gpu):
+    ctx, system, state = _lorenz()
+    traj = M.integrate(system, state, M.StepConfig("0.01", 4), 250, ctx, record_stride=100)
+    assert traj.steps() == [0, 100, 200, 250]
+    assert str(traj.time_of(250)) == "2.50"
+    zero = M.integrate(system, state, M.StepConfig("0.01", 4), 0, ctx)
+    assert zero.steps() == [0] and all(M.mp_bits_equal(a, b) for a, b in zip(zero.points[0].state, state))
+
+
+def test_resume_is_bit_exact_and_runs_are_deterministic(gpu):
+    ctx, system, state = _lorenz()
+    cfg = M.StepConfig("0.01", 10)
+    straight = M.integrate(system, state, cfg, 60, ctx, record_stride=20)
+    again = M.integrate(system, state, cfg, 60, ctx, record_stride=20)
+    head = M.integrate(system, state, cfg, 20, ctx, record_stride=20)
+    resumed = M.integrate(system, head.final_state(), cfg, 60, ctx, record_stride=20, start_step=20)
+    assert resumed.steps() == [20, 40, 60]
+    by_step = {p.step: p.state for p in straight.points}
+    for p in resumed.points:
+        assert all(M.mp_bits_equal(a, b) for a, b in zip(p.state, by_step[p.step]))
+    for a, b in zip(straight.points, again.points):
+        assert all(M.mp_bits_equal(x, y) for x, y in zip(a.state, b.state))
+
+
+def test_observer_sees_every_step(gpu):
+    ctx, system, state = _lorenz()
+    calls = []
+    M.integrate(system, state, M.StepConfig("0.01", 4), 7, ctx,
+                observer=lambda n, t, s: calls.append((n, str(t), type(s))))
+    assert [c[0] for c in calls] == [1, 2, 3, 4, 5, 6, 7]
+    assert calls[0][1] == "0.01" and all(c[2] is tuple for c in calls)
+
+
+def test_compute_jet_hand_values_criterion_1(gpu):
+    ctx, system, state = _lorenz()
+    jet = M.compute_jet(system, state, 2, ctx)
+    ulp = Fraction(1, 2**250)
+    for (m, i), text in {(0, 1): "-16.8", (1, 1): "138.192", (2, 1): "181.144", (0, 2): "774.96"}.items():
+        ref = M.mp_from_decimal(text, ctx).as_fraction()
+        assert abs(jet.coeffs[m][i].as_fraction() - ref) <= ulp * abs(ref)
+    assert all(M.mp_bits_equal(jet.coeffs[m][0], state[m]) for m in range(3))
+
+
+def test_exponential_step_criterion_2(gpu):
+    ctx = M.PrecisionContext(256)
+    system = M.QuadraticODESystem(dim=1, constant=(ctx.zero,), linear=((ctx.one,),), bilinear=((),))
+    (result,) = M.step(system, (ctx.one,), M.StepConfig("1", 30), ctx)
+    e = sum((Fraction(1, math.factorial(n)) for n in range(80)), Fraction(0))
+    assert abs(result.as_fraction() - e) < Fraction(1, 10**32)
+
+
+def test_convergence_order_criterion_3(gpu):
+    ctx = M.PrecisionContext(256)
+    system = M.QuadraticODESystem(dim=1, constant=(ctx.zero,), linear=((ctx.one,),), bilinear=((),))
+    for n in (4, 8):
+        errs = []
+        for tau in ("0.25", "0.125", "0.0625"):
+            (r,) = M.step(system, (ctx.one,), M.StepConfig(tau, n), ctx)
+            x = Fraction(tau)
+            exact = sum((x**k / math.factorial(k) for k in range(90)), Fraction(0))
+            errs.append(abs(r.as_fraction() - exact))
+        for a, b in zip(errs, errs[1:]):
+            assert 2 ** (n + 1) / 4 <= a / b <= 2 ** (n + 1) * 4
+
+
+def test_short_horizon_vs_double_precision_rk_criterion_4(gpu):
+    scipy_integrate = pytest.importorskip("scipy.integrate")
+    ctx, system, state = _lorenz()
+    traj = M.integrate(system, state, M.StepConfig("0.01", 30), 200, ctx)
+    final = [float(v) for v in traj.final_state()]
+
+    def rhs(_t, s):
+        x, y, z = s
+        return [-10.0 * x + 10.0 * y, 28.0 * x - y - x * z, x * y - 8.0 / 3.0 * z]
+
+    sol = scipy_integrate.solve_ivp(rhs, (0.0, 2.0), [float(v) for v in state], method="DOP853",
+                                    rtol=1e-10, atol=1e-12, t_eval=[2.0])
+    for got, ref in zip(final, sol.y[:, -1]):
+        assert abs(got - ref) / abs(ref) < 1e-6
+
+
+def test_overflow_is_reported_not_silent(gpu):
+    ctx = M.PrecisionContext(128)
+    system = M.QuadraticODESystem(dim=1, constant=(ctx.zero,), linear=((ctx.from_int(1000),),), bilinear=((),))
+    with pytest.raises(Exception) as info:
+        M.integrate(system, (ctx.from_int(10**5),), M.StepConfig("1", 20), 3, ctx)
+    assert "range" in str(info.value).lower()

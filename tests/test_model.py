@@ -1,0 +1,102 @@
+"""The device arithmetic (as restated by oracle/fixmodel.c) against the
+reference's frozen outputs: agreement to relative 10^-(K-d) with the
+reference's own metric, d = 3 + ceil(0.3935 t) guard digits (3 digits of
+accumulated rounding plus the Lorenz system's largest Lyapunov exponent,
+0.906 / ln 10 = 0.3935 decimal digits per time unit).
+
+These run on the CPU; the GPU is checked bit for bit against the same model
+in tests/test_gpu.py, so together they carry the parity claim."""
+
+import math
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import paper_1908_09301_b200 as M
+from oracle import fix as FX
+from paper_1908_09301_b200.engine import SystemTables
+from paper_1908_09301_b200.fixed import FixedFormat
+
+from .helpers import agreement_digits, frac, system_from_json
+
+
+def guard_digits(t: float) -> int:
+    return 3 + math.ceil(0.3935 * t)
+
+
+def run_model(case, guard_bits=32):
+    P = case["prec_bits"]
+    ctx = M.PrecisionContext(P)
+    system = system_from_json(case["system"], ctx)
+    fmt = FixedFormat(P, guard_bits)
+    tau = M.mp_from_decimal(case["tau"], ctx)
+    tables = SystemTables.build(system, fmt, case["order"], tau.as_fraction())
+    st = fmt.to_digits([M.mp_from_decimal(t, ctx) for t in case["init"]])
+    steps, recs = FX.integrate(tables, fmt.frac_digits, case["order"], P, st, case["n_steps"], 0, case["stride"])
+    return fmt, steps, recs
+
+
+@pytest.mark.parametrize(
+    "name", ["config0_k50_n40", "cns_pair_128_n20", "cns_pair_256_n30", "config1_k500_n200_3steps",
+             "backward_256_n30"]
+)
+def test_model_matches_reference_within_tolerance(golden, name):
+    c = golden[name]
+    fmt, steps, recs = run_model(c)
+    K = M.decimal_digits(c["prec_bits"])
+    tau = float(Fraction(c["tau"]))
+    assert [int(s) for s in steps] == [r["step"] for r in c["records"]]
+    for r, rec in zip(recs, c["records"]):
+        got = fmt.digits_to_fractions(r)
+        ref = [frac(h) for h in rec["state"]]
+        t = abs(rec["step"] * tau)
+        assert agreement_digits(got, ref) >= K - guard_digits(t), (name, rec["step"])
+
+
+def test_model_states_are_reference_precision_values(golden):
+    """The device rounds the state to P bits each step: every recorded state
+    is a P-bit binary float, like the reference's."""
+    c = golden["config0_k50_n40"]
+    fmt, _, recs = run_model(c)
+    for r in recs[1:]:
+        for f in fmt.digits_to_fractions(r):
+            v = M.MPValue.from_fraction(f, c["prec_bits"])
+            assert v.as_fraction() == f
+
+
+def test_zero_state_is_a_fixed_point(golden):
+    c = golden["zero_state_256_n8"]
+    fmt, _, recs = run_model(c)
+    assert not recs.any()
+
+
+def test_jets_match_reference_jets(golden):
+    """Model jets (tau-scaled by 2^-7, unscaled exactly) vs the reference's
+    jets: each coefficient agrees to the absolute accuracy of the scaled row."""
+    for name, c in golden.items():
+        if c["kind"] != "jet" or c["prec_bits"] > 300:
+            continue
+        P, N = c["prec_bits"], c["order"]
+        ctx = M.PrecisionContext(P)
+        system = system_from_json(c["system"], ctx)
+        fmt = FixedFormat(P)
+        k = 7
+        tables = SystemTables.build(system, fmt, N, Fraction(1, 1 << k))
+        st = fmt.to_digits([frac(h) for h in c["state"]])
+        coef = FX.compute_jet(tables, fmt.frac_digits, N, st)
+        for m in range(system.dim):
+            fr = fmt.digits_to_fractions(coef[m])
+            for i in range(N + 1):
+                ref = frac(c["coeffs"][m][i])
+                got = fr[i] * (1 << (k * i))
+                tol = max(abs(ref), Fraction(1)) * Fraction(1, 2 ** (P - 12)) + Fraction(1 << (k * i), 2 ** (P + 20))
+                assert abs(got - ref) <= tol, (name, m, i)
+
+
+def test_guard_bits_change_nothing_beyond_tolerance(golden):
+    c = golden["config0_k50_n40"]
+    f32, _, r32 = run_model(c, 32)
+    f64, _, r64 = run_model(c, 64)
+    for a, b in zip(r32, r64):
+        assert agreement_digits(f32.digits_to_fractions(a), f64.digits_to_fractions(b)) >= 40
