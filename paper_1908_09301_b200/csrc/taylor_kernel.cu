@@ -107,6 +107,14 @@ struct Acc {
   int64_t v[kR + 1];
 };
 
+// s64 += s32 * s32 as ONE instruction (SASS IMAD.WIDE); writing the product
+// in C++ on int64 operands makes nvcc emit a 64x64 multiply sequence.
+__device__ __forceinline__ int64_t mad_wide(int32_t a, int32_t b, int64_t c) {
+  int64_t d;
+  asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+  return d;
+}
+
 __device__ __forceinline__ void acc_zero(Acc& a) {
 #pragma unroll
   for (int r = 0; r <= kR; r++) a.v[r] = 0;
@@ -164,9 +172,9 @@ __device__ __forceinline__ void mac_group(Acc& acc, int& cnt, const int32_t* __r
 #pragma unroll
     for (int u = 0; u < kR; u++) {
       buf[(kR - u) & (kR - 1)] = bp[-u];
-      int64_t a = ap[u];
+      const int32_t a = ap[u];
 #pragma unroll
-      for (int r = 0; r < kR; r++) acc.v[r] += a * (int64_t)buf[(r - u) & (kR - 1)];
+      for (int r = 0; r < kR; r++) acc.v[r] = mad_wide(a, buf[(r - u) & (kR - 1)], acc.v[r]);
     }
     cnt += kR;
     if (cnt >= kFoldEvery) {
@@ -422,9 +430,12 @@ __global__ void __launch_bounds__(256, 1) taylor_team_kernel(const __grid_consta
         const bool active = slot < ns_a;
         const int c0 = kR * (g.gfb + grp);
         Acc acc[NPT];
+        int cnt[NPT];
 #pragma unroll
-        for (int q = 0; q < NPT; q++) acc_zero(acc[q]);
-        int cnt = 0;
+        for (int q = 0; q < NPT; q++) {
+          acc_zero(acc[q]);
+          cnt[q] = 0;
+        }
         const int nrows = p.nlv + p.nrv;
         for (int k0 = 0; k0 <= i; k0 += p.kc) {
           const int kcn = min(p.kc, i + 1 - k0);
@@ -453,7 +464,7 @@ __global__ void __launch_bounds__(256, 1) taylor_team_kernel(const __grid_consta
                 if (q < p.NP) {
                   const int ra = kk * nrows + p.pl[q];
                   const int rb = kk * nrows + p.nlv + p.pr[q];
-                  mac_group(acc[q], cnt, ROW(stage, ra), stinfo[ra], ROW(stage, rb), stinfo[rb], c0, g.Tb, mc);
+                  mac_group(acc[q], cnt[q], ROW(stage, ra), stinfo[ra], ROW(stage, rb), stinfo[rb], c0, g.Tb, mc);
                 }
               }
             }
@@ -648,24 +659,22 @@ __global__ void __launch_bounds__(256, 1) taylor_team_kernel(const __grid_consta
 // Integer-pipe roofline probe: every thread runs 8 independent IMAD.WIDE
 // chains (s64 += s32 * s32) -- the instruction the Cauchy loop is built on.
 __global__ void imad_wide_probe(int iters, int32_t seed, long long* out) {
-  int64_t a0 = seed, a1 = seed + 1, a2 = seed + 2, a3 = seed + 3, a4 = seed + 4, a5 = seed + 5,
-          a6 = seed + 6, a7 = seed + 7;
+  int64_t acc[8];
+#pragma unroll
+  for (int c = 0; c < 8; c++) acc[c] = seed + c;
   int32_t x = threadIdx.x | 1, y = blockIdx.x | 3;
   for (int i = 0; i < iters; i++) {
 #pragma unroll
     for (int u = 0; u < 8; u++) {
-      a0 += (int64_t)x * y;
-      a1 += (int64_t)(x + 1) * y;
-      a2 += (int64_t)(x + 2) * y;
-      a3 += (int64_t)(x + 3) * y;
-      a4 += (int64_t)(x + 4) * y;
-      a5 += (int64_t)(x + 5) * y;
-      a6 += (int64_t)(x + 6) * y;
-      a7 += (int64_t)(x + 7) * y;
-      y ^= (int32_t)(a0 >> 40);
+#pragma unroll
+      for (int c = 0; c < 8; c++) acc[c] = mad_wide(x + c, y, acc[c]);
+      y += u;
     }
   }
-  if ((a0 ^ a1 ^ a2 ^ a3 ^ a4 ^ a5 ^ a6 ^ a7) == 0x123456789LL) out[0] = a0;
+  int64_t s = 0;
+#pragma unroll
+  for (int c = 0; c < 8; c++) s ^= acc[c];
+  if (s == 0x123456789LL) out[0] = s;
 }
 
 cudaError_t launch_imad_probe(int blocks, int threads, int iters, long long* out, cudaStream_t s) {
