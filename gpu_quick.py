@@ -1,29 +1,20 @@
-import json, time, sys
+import time, sys, os
 import numpy as np
 sys.path.insert(0,'.')
-from oracle import fix as FX
 import paper_1908_09301_b200 as M
 from paper_1908_09301_b200.engine import SystemTables, DevicePlan
 from paper_1908_09301_b200.fixed import FixedFormat
-from fractions import Fraction
-def run(P, N, nsteps, stride, tau='0.01', init=('-15.8','-17.48','35.64')):
-    ctx=M.PrecisionContext(P); sysm=M.builtin_system('lorenz',ctx); fmt=FixedFormat(P)
-    t=M.mp_from_decimal(tau,ctx); tab=SystemTables.build(sysm,fmt,N,t.as_fraction())
-    st=fmt.to_digits([M.mp_from_decimal(x,ctx) for x in init])
-    # jet check
-    cj=FX.compute_jet(tab,fmt.frac_digits,N,st)
-    with DevicePlan(tab,fmt,N,1) as plan:
-        print('plan info',plan.info(), flush=True)
-        gj=plan.compute_jet(st)[0]
-        bad=np.argwhere((gj!=cj).any(axis=2))
-        print(f'P={P} N={N} jet mismatches:', len(bad), bad[:5].tolist(), flush=True)
-        if len(bad):
-            m,i=bad[0]; print(' first gpu',gj[m,i][:12].tolist(),'\n first cpu',cj[m,i][:12].tolist())
-        t0=time.time(); steps,recs,status=plan.integrate(st,nsteps,0,stride); dt=time.time()-t0
-        cs,cr=FX.integrate(tab,fmt.frac_digits,N,P,st,nsteps,0,stride)
-        eq=(recs[:,0]==cr).all(axis=(1,2))
-        print(f'  integrate {nsteps} steps: wall {dt:.3f}s kernel {plan.last_kernel_ms():.3f}ms status {status.tolist()} records equal: {eq.tolist()}', flush=True)
-run(167,40,50,10)
-run(256,30,20,5)
-run(1661,200,3,1)
-run(1661,200,20,10)
+def perf(K, N, steps, configs):
+    P=M.bits_for_digits(K); ctx=M.PrecisionContext(P); sysm=M.builtin_system('lorenz',ctx); fmt=FixedFormat(P)
+    tab=SystemTables.build(sysm,fmt,N,M.mp_from_decimal('0.01',ctx).as_fraction())
+    st=fmt.to_digits([M.mp_from_decimal(x,ctx) for x in ('-15.8','-17.48','35.64')])
+    for kern, G in configs:
+        with DevicePlan(tab,fmt,N,1) as plan:
+            try: plan.configure(kern, G)
+            except Exception as e: print(kern,G,'unavailable',e); continue
+            plan.upload(st); plan.run_device(2); plan.last_kernel_ms()
+            plan.count_macs(True); plan.run_device(steps); ms=plan.last_kernel_ms(); u,x=plan.read_macs()
+            print(f'K={K} N={N} {plan.info()} : {ms/steps:.3f} ms/step = {1000*steps/ms:.1f} steps/s; useful MAC/step {u/steps:.3e} executed {x/steps:.3e}', flush=True)
+perf(50,40,100,[('team',1),('cluster',1),('cluster',2),('cluster',4),('cluster',8),('cluster',16)])
+perf(500,200,20,[('team',1),('cluster',1),('cluster',2),('cluster',4),('cluster',8),('cluster',16)])
+perf(800,480,2,[('team',1),('cluster',4),('cluster',8),('cluster',16)])

@@ -16,9 +16,11 @@
  *   tprod(A, C, T) = sum_{p+q >= T} a_p c_q B^(p+q-T)   (truncated product)
  *   rnd(V)         = floor((V + B^2/2) / B^2)          (two guard digits)
  *
- *   order i:  S_p  = rnd( sum_k tprod(coef[j_p][i-k], coef[k_p][k], Lf-2) )
+ *   order i:  V_p  = sum_k tprod(coef[j_p][i-k], coef[k_p][k], Lf-2)   (exact)
  *             U_m  = rnd( [i==0] cst_m B^2 + sum_j tprod(lin[m][j], coef[j][i], Lf-2)
- *                                          + sum_t tprod(q_t, S_{p_t}, Lf-2) )
+ *                         + sum_t Q_t )
+ *             Q_t  = q_t * V_{p_t}                 if q_t is a small integer
+ *                    tprod(q_t, rnd(V_{p_t}), Lf-2) otherwise
  *             coef[m][i+1] = rnd( tprod(U_m, Ctab[i], Lf+sc-2) ),
  *   Ctab[i] = round(tau * 2^(F + 28 sc) / (i+1)) computed on the host.
  *   state'[m] = RN_P( sum_i coef[m][i] )  (exact sum, then ties-to-even
@@ -137,28 +139,54 @@ static int build(model_t *M, int D, int NT, const int32_t *teq, const int32_t *t
   return 0;
 }
 
+/* a constant is a "small integer" when only its integer digit (index Lf) is
+   nonzero and |d_Lf| <= 4096; bilinear terms with such coefficients are
+   applied to the exact Cauchy column sum (no intermediate rounding) */
+static int small_int(const int32_t *v, int Lf, int64_t *out) {
+  for (int j = 0; j < Lf; j++)
+    if (v[j]) return 0;
+  if (v[Lf] > 4096 || v[Lf] < -4096) return 0;
+  *out = v[Lf];
+  return 1;
+}
+
 /* coef: D x (order+1) x W, coef[m][0] set by caller */
 static int jet(const model_t *M, int32_t *coef) {
   int Lf = M->Lf, L = Lf + 1, Wd = W(M), D = M->D, N = M->order;
   int ncols = Lf + 3; /* columns [Lf-2, 2Lf] */
   i128 *col = malloc(sizeof(i128) * (size_t)(ncols + 2));
+  i128 *V = malloc(sizeof(i128) * (size_t)(M->NP + 1) * ncols);
   int32_t *S = malloc(sizeof(int32_t) * (size_t)(M->NP + 1) * Wd);
   int32_t *U = malloc(sizeof(int32_t) * (size_t)D * Wd);
+  int64_t qint[64];
+  int qsmall[64];
+  for (int t = 0; t < M->NT; t++) qsmall[t] = small_int(M->q + (size_t)t * Wd, Lf, &qint[t]);
   int rc = 0;
 #define CO(m, i) (coef + ((size_t)(m) * (N + 1) + (i)) * Wd)
   for (int i = 0; i < N && !rc; i++) {
     for (int p = 0; p < M->NP; p++) {
-      memset(col, 0, sizeof(i128) * ncols);
-      for (int k = 0; k <= i; k++) tprod_acc(CO(M->pj[p], i - k), CO(M->pk[p], k), L, Lf - 2, col, ncols);
-      if (round_cols(col, ncols, Lf, S + (size_t)p * Wd)) rc = 1;
+      i128 *vp = V + (size_t)p * ncols;
+      memset(vp, 0, sizeof(i128) * ncols);
+      for (int k = 0; k <= i; k++) tprod_acc(CO(M->pj[p], i - k), CO(M->pk[p], k), L, Lf - 2, vp, ncols);
+      int need = 0;
+      for (int t = 0; t < M->NT; t++)
+        if (M->tpair[t] == p && !qsmall[t]) need = 1;
+      if (need && round_cols(vp, ncols, Lf, S + (size_t)p * Wd)) rc = 1;
     }
     for (int m = 0; m < D; m++) {
       memset(col, 0, sizeof(i128) * ncols);
       if (i == 0)
         for (int j = 0; j <= Lf; j++) col[2 + j] += (i128)M->cst[(size_t)m * Wd + j];
       for (int j = 0; j < D; j++) tprod_acc(M->lin + ((size_t)m * D + j) * Wd, CO(j, i), L, Lf - 2, col, ncols);
-      for (int t = 0; t < M->NT; t++)
-        if (M->teq[t] == m) tprod_acc(M->q + (size_t)t * Wd, S + (size_t)M->tpair[t] * Wd, L, Lf - 2, col, ncols);
+      for (int t = 0; t < M->NT; t++) {
+        if (M->teq[t] != m) continue;
+        if (qsmall[t]) {
+          const i128 *vp = V + (size_t)M->tpair[t] * ncols;
+          for (int c = 0; c < ncols; c++) col[c] += (i128)qint[t] * vp[c];
+        } else {
+          tprod_acc(M->q + (size_t)t * Wd, S + (size_t)M->tpair[t] * Wd, L, Lf - 2, col, ncols);
+        }
+      }
       if (round_cols(col, ncols, Lf, U + (size_t)m * Wd)) rc = 1;
     }
     for (int m = 0; m < D; m++) {
@@ -168,6 +196,7 @@ static int jet(const model_t *M, int32_t *coef) {
     }
   }
   free(col);
+  free(V);
   free(S);
   free(U);
   return rc;

@@ -32,6 +32,8 @@ EXPORTS = (
     "mpt_step",
     "mpt_last_kernel_ms",
     "mpt_plan_info",
+    "mpt_plan_configure",
+    "mpt_plan_kernel",
     "mpt_count_macs",
     "mpt_read_macs",
     "mpt_imad_probe",
@@ -75,6 +77,8 @@ def _declare(L):
     L.mpt_last_kernel_ms.argtypes = [vp]
     L.mpt_last_kernel_ms.restype = ctypes.c_float
     L.mpt_plan_info.argtypes = [vp, i32p, i32p, i32p]
+    L.mpt_plan_configure.argtypes = [vp, ctypes.c_int, ctypes.c_int]
+    L.mpt_plan_kernel.argtypes = [vp, i32p, i32p]
     u64p = ctypes.POINTER(ctypes.c_ulonglong)
     L.mpt_count_macs.argtypes = [vp, ctypes.c_int]
     L.mpt_read_macs.argtypes = [vp, u64p, u64p]

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -14,6 +15,9 @@ namespace mpt {
 size_t smem_bytes(const Params& p);
 cudaError_t launch_team_kernel(const Params& p, size_t smem, cudaStream_t stream);
 cudaError_t launch_imad_probe(int blocks, int threads, int iters, long long* out, cudaStream_t s);
+size_t cluster_smem_bytes(const Params& p, int G);
+cudaError_t launch_cluster_kernel(const Params& p, int G, size_t smem, cudaStream_t stream);
+int max_cluster_size(const Params& p, size_t smem, int want);
 }  // namespace mpt
 
 static thread_local std::string g_err;
@@ -44,7 +48,37 @@ struct mpt_plan {
   bool have_constants = false;
   unsigned long long* d_counters = nullptr;
   bool counting = false;
+  int kernel = 0;    // 1 = team kernel (rows in HBM/L2), 2 = cluster kernel (rows in smem)
+  int cluster = 1;   // CTAs per trajectory for the cluster kernel
+  size_t smem_cluster = 0;
+  int optin = 0;
 };
+
+// choose the kernel: the smem-resident cluster kernel when the rows fit,
+// one cluster of `want` CTAs per trajectory (clamped to what co-schedules)
+static int choose_kernel(mpt_plan* pl, int kernel, int want) {
+  mpt::Params& p = pl->p;
+  if (kernel == 1) {
+    pl->kernel = 1;
+    pl->cluster = 1;
+    return MPT_OK;
+  }
+  const int tries[] = {16, 8, 4, 2, 1};
+  for (int G : tries) {
+    if (G > want) continue;
+    size_t s = mpt::cluster_smem_bytes(p, G);
+    if (s > (size_t)pl->optin) continue;
+    if (G > 1 && mpt::max_cluster_size(p, s, G) < 1) continue;
+    pl->kernel = 2;
+    pl->cluster = G;
+    pl->smem_cluster = s;
+    return MPT_OK;
+  }
+  if (kernel == 2) return fail(MPT_EUNSUP, "coefficient rows do not fit shared memory for the cluster kernel");
+  pl->kernel = 1;
+  pl->cluster = 1;
+  return MPT_OK;
+}
 
 extern "C" {
 
@@ -139,6 +173,7 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
   }
   int optin = 0;
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  pl->optin = optin;
   // largest k-chunk that fits in shared memory
   size_t smem = 0;
   int kc = 64;
@@ -181,7 +216,30 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
   p.rinfo = pl->d_rinfo;
   p.state = pl->d_state;
   p.status = pl->d_status;
+  {
+    const char* ek = getenv("MPT_KERNEL");
+    const char* ec = getenv("MPT_CLUSTER");
+    int kernel = ek ? (strcmp(ek, "team") == 0 ? 1 : strcmp(ek, "cluster") == 0 ? 2 : 0) : 0;
+    int want = ec ? atoi(ec) : (n_traj == 1 ? 8 : 1);
+    int rc = choose_kernel(pl, kernel, want < 1 ? 1 : want);
+    if (rc) {
+      mpt_plan_destroy(pl);
+      return rc;
+    }
+  }
   *out = pl;
+  return MPT_OK;
+}
+
+int mpt_plan_configure(mpt_plan* pl, int kernel, int cluster) {
+  if (!pl || kernel < 0 || kernel > 2 || cluster < 1 || cluster > 16) return fail(MPT_EINVAL, "bad configuration");
+  return choose_kernel(pl, kernel, cluster);
+}
+
+int mpt_plan_kernel(const mpt_plan* pl, int* kernel, int* cluster) {
+  if (!pl) return MPT_EINVAL;
+  if (kernel) *kernel = pl->kernel;
+  if (cluster) *cluster = pl->cluster;
   return MPT_OK;
 }
 
@@ -207,7 +265,7 @@ int mpt_plan_width(const mpt_plan* pl) { return pl ? pl->W : MPT_EINVAL; }
 
 int mpt_plan_info(const mpt_plan* pl, int* smem_bytes, int* k_chunk, int* threads) {
   if (!pl) return MPT_EINVAL;
-  if (smem_bytes) *smem_bytes = (int)pl->smem;
+  if (smem_bytes) *smem_bytes = (int)(pl->kernel == 2 ? pl->smem_cluster : pl->smem);
   if (k_chunk) *k_chunk = pl->p.kc;
   if (threads) *threads = pl->p.nthreads;
   return MPT_OK;
@@ -238,6 +296,27 @@ int mpt_plan_set_constants(mpt_plan* pl, const int32_t* cst, const int32_t* lin,
   if ((rc = upload_rows(pl->d_lin, lin, (size_t)p.D * p.D, p.W, p.RS))) return rc;
   if (p.NT > 0 && (rc = upload_rows(pl->d_q, q, p.NT, p.W, p.RS))) return rc;
   if ((rc = upload_rows(pl->d_ctab, ctab, p.N, p.W, p.RS))) return rc;
+  // small-integer coefficients (oracle/fixmodel.c small_int)
+  auto small = [&](const int32_t* v, int* out) {
+    for (int j = 0; j < p.Lf; j++)
+      if (v[j]) return 0;
+    if (v[p.Lf] > 4096 || v[p.Lf] < -4096) return 0;
+    *out = v[p.Lf];
+    return 1;
+  };
+  mpt::Params& pm = pl->p;
+  for (int e = 0; e < p.D * p.D; e++) {
+    int val = 0;
+    pm.lin_small[e] = small(lin + (size_t)e * p.W, &val);
+    pm.lin_int[e] = val;
+  }
+  for (int r = 0; r < p.NP; r++) pm.pair_round[r] = 0;
+  for (int t = 0; t < p.NT; t++) {
+    int val = 0;
+    pm.tq_small[t] = small(q + (size_t)t * p.W, &val);
+    pm.tq_int[t] = val;
+    if (!pm.tq_small[t]) pm.pair_round[p.tpair[t]] = 1;
+  }
   pl->have_constants = true;
   return MPT_OK;
 }
@@ -259,7 +338,10 @@ static int launch(mpt_plan* pl, int n_steps, int start_step, int stride, cudaStr
   p.rec = pl->d_rec;
   p.counters = pl->counting ? pl->d_counters : nullptr;
   CK(cudaEventRecord(pl->ev0, stream));
-  CK(mpt::launch_team_kernel(p, pl->smem, stream));
+  if (pl->kernel == 2)
+    CK(mpt::launch_cluster_kernel(p, pl->cluster, pl->smem_cluster, stream));
+  else
+    CK(mpt::launch_team_kernel(p, pl->smem, stream));
   CK(cudaEventRecord(pl->ev1, stream));
   return MPT_OK;
 }

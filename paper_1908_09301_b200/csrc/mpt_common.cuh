@@ -36,6 +36,12 @@ struct Params {
   int nlv, nrv;               // distinct left / right variables of the pairs
   int lvar[kMaxP], rvar[kMaxP];
   int pl[kMaxP], pr[kMaxP];   // pair -> index into lvar / rvar
+  // bilinear coefficients that are small integers are applied to the exact
+  // Cauchy column sums (no intermediate rounding); pairs used by any other
+  // term are rounded first (oracle/fixmodel.c small_int)
+  int tq_small[kMaxT], tq_int[kMaxT];
+  int pair_round[kMaxP];
+  int lin_small[kMaxD * kMaxD], lin_int[kMaxD * kMaxD];
   // constants (global, row stride RS)
   const int32_t* cst;   // D rows
   const int32_t* lin;   // D*D rows

@@ -22,6 +22,7 @@
 #include <cstdint>
 
 #include "mpt_common.cuh"
+#include "mpt_device.cuh"
 
 namespace mpt {
 
@@ -90,240 +91,11 @@ __host__ __device__ inline Layout make_layout(const Params& p) {
   L.off_ct = take(sizeof(int32_t) * (size_t)L.rw);
   L.off_ctinf = take(sizeof(int2));
   L.off_part = take(sizeof(int64_t) * (size_t)L.n_units * g.NCX);
-  int nout = p.NP > p.D ? p.NP : p.D;
-  L.off_col = take(sizeof(int64_t) * (size_t)nout * g.NCX);
+  L.off_col = take(sizeof(int64_t) * (size_t)(p.NP + p.D) * g.NCX);  // V_p then U_m
   L.off_uout = take(sizeof(int) * (size_t)L.n_units);
   L.off_flag = take(sizeof(int) * 4);
   L.total = o;
   return L;
-}
-
-// ---------------------------------------------------------------------------
-// Column accumulation for one (operand pair, column group).
-// acc[r] += sum_p A[p] * B[c0 + r - p] for the group's absolute columns
-// c0..c0+kR-1; acc[kR] collects the carries of folds. Rows are padded with
-// kPad zeros on both sides so the register window never needs bounds checks.
-struct Acc {
-  int64_t v[kR + 1];
-};
-
-// s64 += s32 * s32 as ONE instruction (SASS IMAD.WIDE); writing the product
-// in C++ on int64 operands makes nvcc emit a 64x64 multiply sequence.
-__device__ __forceinline__ int64_t mad_wide(int32_t a, int32_t b, int64_t c) {
-  int64_t d;
-  asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
-  return d;
-}
-
-__device__ __forceinline__ void acc_zero(Acc& a) {
-#pragma unroll
-  for (int r = 0; r <= kR; r++) a.v[r] = 0;
-}
-
-// fold: digits of acc[0..kR-1] into [0, B), carries ripple upward into acc[kR].
-// Columns below `tcut` (absolute) are discarded first: products there are
-// outside the truncated product and must not leak carries upward.
-__device__ __forceinline__ void acc_fold(Acc& a, int c0, int tcut) {
-#pragma unroll
-  for (int r = 0; r < kR; r++) {
-    if (c0 + r < tcut) a.v[r] = 0;
-    int64_t c = a.v[r] >> kRadixBits;
-    a.v[r] &= kMask;
-    a.v[r + 1] += c;
-  }
-}
-
-struct MacCount {
-  unsigned long long useful = 0, executed = 0;
-};
-
-// exact number of digit products (p, q) inside the nonzero windows that fall
-// in the group's kept columns [max(c0, tcut), c0 + kR) -- the algorithmic work
-__device__ __forceinline__ unsigned useful_macs(int2 ia, int2 ib, int c0, int tcut) {
-  unsigned n = 0;
-#pragma unroll
-  for (int r = 0; r < kR; r++) {
-    int c = c0 + r;
-    int lo = max(ia.x, c - ib.y), hi = min(ia.y, c - ib.x);
-    if (c >= tcut && hi >= lo) n += hi - lo + 1;
-  }
-  return n;
-}
-
-__device__ __forceinline__ void mac_group(Acc& acc, int& cnt, const int32_t* __restrict__ A, int2 ia,
-                                          const int32_t* __restrict__ B, int2 ib, int c0, int tcut,
-                                          MacCount* mc = nullptr) {
-  // nonzero digits: A in [ia.x, ia.y], B in [ib.x, ib.y]
-  int plo = max(ia.x, c0 - ib.y);
-  int phi = min(ia.y, c0 + kR - 1 - ib.x);
-  if (plo > phi) return;
-  int P0 = plo & ~(kR - 1);
-  if (mc) {
-    mc->useful += useful_macs(ia, ib, c0, tcut);
-    mc->executed += (unsigned long long)(((phi - P0) / kR + 1) * kR * kR);
-  }
-  int32_t buf[kR];
-  const int32_t* bq = B + (c0 - P0);  // bq[s] = B[c0 - P0 + s]
-#pragma unroll
-  for (int s = 1; s < kR; s++) buf[s] = bq[s];
-  for (; P0 <= phi; P0 += kR) {
-    const int32_t* ap = A + P0;
-    const int32_t* bp = B + (c0 - P0);
-#pragma unroll
-    for (int u = 0; u < kR; u++) {
-      buf[(kR - u) & (kR - 1)] = bp[-u];
-      const int32_t a = ap[u];
-#pragma unroll
-      for (int r = 0; r < kR; r++) acc.v[r] = mad_wide(a, buf[(r - u) & (kR - 1)], acc.v[r]);
-    }
-    cnt += kR;
-    if (cnt >= kFoldEvery) {
-      acc_fold(acc, c0, tcut);
-      cnt = 0;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Warp-cooperative normalisation of a column vector (relative columns
-// 0..ncols-1, value V = sum col[c] B^c) into canonical signed digits of
-// floor((V + shift_half) / B^drop), drop in {0, 2}. Output digits j = 0..W-1
-// go to `out` (a padded shared row), bot/top of nonzero digits to *info.
-// Returns true on overflow. Runs on one full warp.
-__device__ __forceinline__ void warp_carry(int64_t (&v)[kMaxLanesDigits], int m, int64_t& top) {
-  const unsigned full = 0xffffffffu;
-  int lane = threadIdx.x & 31;
-  int64_t c = 0;
-#pragma unroll
-  for (int j = 0; j < kMaxLanesDigits; j++) {
-    if (j < m) {
-      int64_t t = v[j] + c;
-      int64_t d = t & kMask;
-      c = (t - d) >> kRadixBits;
-      v[j] = d;
-    }
-  }
-  while (__any_sync(full, c != 0)) {
-    int64_t cin = __shfl_up_sync(full, c, 1);
-    if (lane == 0) cin = 0;
-    if (lane == 31) top += c;
-    c = 0;
-    if (cin != 0) {
-#pragma unroll
-      for (int j = 0; j < kMaxLanesDigits; j++) {
-        if (j < m) {
-          int64_t t = v[j] + cin;
-          int64_t d = t & kMask;
-          cin = (t - d) >> kRadixBits;
-          v[j] = d;
-        }
-      }
-      c = cin;
-    }
-  }
-  top = __shfl_sync(full, top, 31);
-}
-
-__device__ void round_to_prec(int32_t* out, int W, int prec_bits, bool& ovf) {
-  // lane-0 sequential: round the canonical digit vector to prec_bits
-  // significant bits, ties to even (the reference's state precision).
-  int tp = -1;
-  for (int d = W - 1; d >= 0; d--)
-    if (out[d]) {
-      tp = d;
-      break;
-    }
-  if (tp < 0) return;
-  const bool neg = out[tp] < 0;
-  auto mag = [&](int d) -> int32_t { return out[d] < 0 ? -out[d] : out[d]; };
-  const int nbits = kRadixBits * tp + (32 - __clz(mag(tp)));
-  const int s = nbits - prec_bits;  // number of low bits to drop
-  if (s <= 0) return;
-  const int sd = s / kRadixBits, sb = s % kRadixBits;
-  const int hp = s - 1, hd = hp / kRadixBits, hb = hp % kRadixBits;
-  const bool half = (mag(hd) >> hb) & 1;
-  const bool lsb = (mag(sd) >> sb) & 1;
-  bool sticky = (mag(hd) & ((1 << hb) - 1)) != 0;
-  for (int d = 0; d < hd && !sticky; d++) sticky = out[d] != 0;
-  for (int d = 0; d < sd; d++) out[d] = 0;
-  int64_t m = mag(sd) & ~((int64_t(1) << sb) - 1);
-  int64_t cin = (half && (sticky || lsb)) ? (int64_t(1) << sb) : 0;
-  for (int d = sd; d < W; d++) {
-    if (d > sd) {
-      if (!cin) break;
-      m = mag(d);
-    }
-    m += cin;
-    cin = m >> kRadixBits;
-    m &= kMask;
-    out[d] = (int32_t)(neg ? -m : m);
-  }
-  if (cin) ovf = true;
-}
-
-__device__ bool warp_normalize(const int64_t* col, int ncols, int drop, int W, int32_t* out, int2* info,
-                               int round_prec_bits) {
-  const unsigned full = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  const int m = (ncols + 31) / 32;
-  int64_t v[kMaxLanesDigits];
-#pragma unroll
-  for (int j = 0; j < kMaxLanesDigits; j++) {
-    int c = lane * m + j;
-    v[j] = (j < m && c < ncols) ? col[c] : 0;
-  }
-  int64_t top = 0;
-  warp_carry(v, m, top);  // digits in [0, B), signed carry in `top`
-  if (drop) {
-    // floor((V + B^drop/2) / B^drop): add B/2 at column drop-1, propagate,
-    // then discard the (non-negative) low digits.
-#pragma unroll
-    for (int j = 0; j < kMaxLanesDigits; j++)
-      if (lane * m + j == drop - 1) v[j] += kRadix / 2;
-    warp_carry(v, m, top);
-#pragma unroll
-    for (int j = 0; j < kMaxLanesDigits; j++)
-      if (lane * m + j < drop) v[j] = 0;
-  }
-  const bool neg = top < 0;
-  if (neg) {  // magnitude of a negative result: negate and renormalise
-#pragma unroll
-    for (int j = 0; j < kMaxLanesDigits; j++) v[j] = -v[j];
-    top = -top;
-    warp_carry(v, m, top);
-  }
-  bool ovf = top != 0;
-#pragma unroll
-  for (int j = 0; j < kMaxLanesDigits; j++) {
-    int c = lane * m + j;
-    if (j < m && c >= drop && c < ncols) {
-      int d = c - drop;
-      int32_t dig = (int32_t)v[j];
-      if (d < W)
-        out[d] = neg ? -dig : dig;
-      else if (dig)
-        ovf = true;
-    }
-  }
-  for (int d = ncols - drop + lane; d < W; d += 32) out[d] = 0;
-  ovf = __any_sync(full, ovf);
-  __syncwarp();
-  if (round_prec_bits > 0) {
-    if (lane == 0) round_to_prec(out, W, round_prec_bits, ovf);
-    ovf = __shfl_sync(full, ovf, 0);
-    __syncwarp();
-  }
-  int bot = 1 << 30, tp = -1;
-  for (int d = lane; d < W; d += 32)
-    if (out[d]) {
-      bot = min(bot, d);
-      tp = max(tp, d);
-    }
-  bot = __reduce_min_sync(full, bot);
-  tp = __reduce_max_sync(full, tp);
-  if (lane == 0) *info = make_int2(tp >= 0 ? bot : W, tp);
-  __syncwarp();
-  return ovf;
 }
 
 // ---------------------------------------------------------------------------
@@ -510,6 +282,7 @@ __global__ void __launch_bounds__(256, 1) taylor_team_kernel(const __grid_consta
         __syncthreads();
         for (size_t w = tid; w < (size_t)ns_a * p.NP * g.NCX; w += nt) part[w] = 0;
         for (int q = warp; q < p.NP; q += nwarps) {
+          if (!p.pair_round[q]) continue;
           bool o = warp_normalize(colsum + (size_t)q * g.NCX, ncol, 2, p.W, ROW(srow, q), &sinf[q], 0);
           if (o && (tid & 31) == 0) flag[0] = 1;
         }
@@ -517,17 +290,17 @@ __global__ void __launch_bounds__(256, 1) taylor_team_kernel(const __grid_consta
       }
       // ===================== phase B: numerators =====================
       {
-        // items: lin (m, j) for nonzero L_mj, then bilinear terms
+        // product items: non-small-integer linear coefficients and non-small-integer q terms
         const int nlin = p.D * p.D;
         const int nitems = nlin + p.NT;
         for (int u = tid; u < nitems; u += nt) uout[u] = u < nlin ? u / p.D : p.teq[u - nlin];
-        // every thread: (item, grp)
         for (int e = tid; e < nitems * g.NGb; e += nt) {
           const int it = e / g.NGb, grp = e % g.NGb;
           const int c0 = kR * (g.gfb + grp);
           const int32_t *A, *B;
           int2 ia, ib;
           if (it < nlin) {
+            if (p.lin_small[it]) continue;
             const int m = it / p.D, j = it % p.D;
             A = ROW(crow, p.D + m * p.D + j);
             ia = cinfo[p.D + m * p.D + j];
@@ -535,6 +308,7 @@ __global__ void __launch_bounds__(256, 1) taylor_team_kernel(const __grid_consta
             ib = curinfo[j];
           } else {
             const int t = it - nlin;
+            if (p.tq_small[t]) continue;
             A = ROW(crow, p.D + nlin + t);
             ia = cinfo[p.D + nlin + t];
             B = ROW(srow, p.tpair[t]);
@@ -554,20 +328,28 @@ __global__ void __launch_bounds__(256, 1) taylor_team_kernel(const __grid_consta
         }
         __syncthreads();
         const int ncol = kR * (g.gfb + g.NGb) - g.Tb + 1;
+        int64_t* ucol = colsum + (size_t)p.NP * g.NCX;
         for (int e = tid; e < p.D * ncol; e += nt) {
-          int m = e / ncol, c = e % ncol;
+          const int m = e / ncol, c = e % ncol;
           int64_t s = 0;
           for (int u = 0; u < nitems; u++)
             if (uout[u] == m) s += part[(size_t)u * g.NCX + c];
-          if (i == 0 && c >= 2 && c - 2 < p.W) s += ROW(crow, m)[c - 2];
-          colsum[(size_t)m * g.NCX + c] = s;
+          if (c >= 2 && c - 2 < p.W) {
+            const int dgt = c - 2;
+            if (i == 0) s += ROW(crow, m)[dgt];
+            for (int j = 0; j < p.D; j++)
+              if (p.lin_small[m * p.D + j]) s += (int64_t)p.lin_int[m * p.D + j] * ROW(cur, j)[dgt];
+          }
+          for (int t = 0; t < p.NT; t++)
+            if (p.teq[t] == m && p.tq_small[t]) s += (int64_t)p.tq_int[t] * colsum[(size_t)p.tpair[t] * g.NCX + c];
+          ucol[(size_t)m * g.NCX + c] = s;
         }
         __syncthreads();
         for (size_t w = tid; w < (size_t)nitems * g.NCX; w += nt) part[w] = 0;
         // tau/(i+1) row for phase C
         copy_row(ROW(ctrow, 0), p.ctab + (size_t)i * p.RS, p.RS);
         for (int m = warp; m < p.D; m += nwarps) {
-          bool o = warp_normalize(colsum + (size_t)m * g.NCX, ncol, 2, p.W, ROW(urow, m), &uinf[m], 0);
+          bool o = warp_normalize(ucol + (size_t)m * g.NCX, ncol, 2, p.W, ROW(urow, m), &uinf[m], 0);
           if (o && (tid & 31) == 0) flag[0] = 1;
         }
         __syncthreads();

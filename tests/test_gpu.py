@@ -49,6 +49,21 @@ def test_integrate_bit_exact_vs_model(gpu, P, N, steps, stride):
     assert np.array_equal(r_gpu[:, 0], r_cpu)
 
 
+@pytest.mark.parametrize("kernel,cluster", [("team", 1), ("cluster", 1), ("cluster", 2), ("cluster", 8),
+                                            ("cluster", 16)])
+@pytest.mark.parametrize("P,N,steps", [(167, 40, 12), (1661, 200, 2)])
+def test_every_kernel_bit_exact_vs_model(gpu, kernel, cluster, P, N, steps):
+    ctx, system, fmt, tables = lorenz_tables(P, N)
+    st = fmt.to_digits([M.mp_from_decimal(t, ctx) for t in CANON_INIT])
+    with DevicePlan(tables, fmt, N, 1) as plan:
+        plan.configure(kernel, cluster)
+        info = plan.info()
+        assert info["kernel"] == kernel
+        s_gpu, r_gpu, status = plan.integrate(st, steps, 0, 1)
+    s_cpu, r_cpu = FX.integrate(tables, fmt.frac_digits, N, P, st, steps, 0, 1)
+    assert np.array_equal(r_gpu[:, 0], r_cpu), info
+
+
 def test_jet_bit_exact_vs_model_large_order(gpu):
     P, N = 1661, 200
     ctx, system, fmt, tables = lorenz_tables(P, N)
