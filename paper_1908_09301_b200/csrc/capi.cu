@@ -311,11 +311,15 @@ int mpt_plan_set_constants(mpt_plan* pl, const int32_t* cst, const int32_t* lin,
     pm.lin_int[e] = val;
   }
   for (int r = 0; r < p.NP; r++) pm.pair_round[r] = 0;
+  pm.all_q_small = 1;
   for (int t = 0; t < p.NT; t++) {
     int val = 0;
     pm.tq_small[t] = small(q + (size_t)t * p.W, &val);
     pm.tq_int[t] = val;
-    if (!pm.tq_small[t]) pm.pair_round[p.tpair[t]] = 1;
+    if (!pm.tq_small[t]) {
+      pm.pair_round[p.tpair[t]] = 1;
+      pm.all_q_small = 0;
+    }
   }
   pl->have_constants = true;
   return MPT_OK;

@@ -41,6 +41,7 @@ struct Params {
   // term are rounded first (oracle/fixmodel.c small_int)
   int tq_small[kMaxT], tq_int[kMaxT];
   int pair_round[kMaxP];
+  int all_q_small;
   int lin_small[kMaxD * kMaxD], lin_int[kMaxD * kMaxD];
   // constants (global, row stride RS)
   const int32_t* cst;   // D rows

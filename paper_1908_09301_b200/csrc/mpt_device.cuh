@@ -101,42 +101,152 @@ __device__ __forceinline__ void mac_group(Acc& acc, int& cnt, const int32_t* __r
 
 // ---------------------------------------------------------------------------
 // Warp-cooperative normalisation of a column vector (relative columns
-// 0..ncols-1, value V = sum col[c] B^c) into canonical signed digits of
-// floor((V + shift_half) / B^drop), drop in {0, 2}. Output digits j = 0..W-1
-// go to `out` (a padded shared row), bot/top of nonzero digits to *info.
-// Returns true on overflow. Runs on one full warp.
-__device__ __forceinline__ void warp_carry(int64_t (&v)[kMaxLanesDigits], int m, int64_t& top) {
-  const unsigned full = 0xffffffffu;
-  int lane = threadIdx.x & 31;
-  int64_t c = 0;
+// 0..ncols-1, value V = sum col[c] B^c, |col[c]| < 2^62) into canonical signed
+// digits of floor((V + [drop] B^drop / 2) / B^drop), drop in {0, 2}.
+// Lane l holds columns [l*m, l*m+m). Carries are resolved without
+// data-dependent loops: one local pass, two shuffle passes (carries shrink to
+// {-1, 0, +1}), then a ballot carry-lookahead per sign:
+//   carry-in mask C = (((A & P) + P) ^ P) | A,  A = lanes receiving a carry,
+//   P = lanes whose block would pass it on (all digits B-1, or all 0 for borrows).
+template <int MM>
+struct Blk {
+  int64_t v[MM];
+};
+
+// add `cin` to the block (digit 0 upward); digits back to [0, B); returns carry out
+template <int MM>
+__device__ __forceinline__ int64_t blk_add(Blk<MM>& b, int m, int64_t cin) {
 #pragma unroll
-  for (int j = 0; j < kMaxLanesDigits; j++) {
+  for (int j = 0; j < MM; j++) {
     if (j < m) {
-      int64_t t = v[j] + c;
-      int64_t d = t & kMask;
-      c = (t - d) >> kRadixBits;
-      v[j] = d;
+      const int64_t t = b.v[j] + cin;
+      const int64_t dgt = t & kMask;
+      cin = (t - dgt) >> kRadixBits;
+      b.v[j] = dgt;
     }
   }
-  while (__any_sync(full, c != 0)) {
-    int64_t cin = __shfl_up_sync(full, c, 1);
-    if (lane == 0) cin = 0;
-    if (lane == 31) top += c;
-    c = 0;
-    if (cin != 0) {
+  return cin;
+}
+
+template <int MM>
+__device__ __forceinline__ bool blk_all(const Blk<MM>& b, int m, int64_t val) {
+  bool all = true;
 #pragma unroll
-      for (int j = 0; j < kMaxLanesDigits; j++) {
+  for (int j = 0; j < MM; j++)
+    if (j < m) all &= (b.v[j] == val);
+  return all;
+}
+
+// resolve pending carries e (from this lane into the next) in {-1, 0, 1};
+// `top` collects what leaves lane 31
+template <int MM>
+__device__ __forceinline__ void blk_resolve(Blk<MM>& b, int m, int e, int64_t& top) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int ein = __shfl_up_sync(full, e, 1);
+  const int e31 = __shfl_sync(full, e, 31);
+  top += e31;
+#pragma unroll
+  for (int sgn = 1; sgn >= -1; sgn -= 2) {
+    const unsigned A = __ballot_sync(full, lane > 0 && ein == sgn);
+    const unsigned P = __ballot_sync(full, blk_all(b, m, sgn > 0 ? kMask : 0));
+    const unsigned long long S = (unsigned long long)(A & P) + P;
+    const unsigned C = ((unsigned)S ^ P) | A;
+    top += sgn * (int64_t)(S >> 32);
+    if ((C >> lane) & 1u) blk_add(b, m, sgn);
+  }
+}
+
+template <int MM>
+__device__ __forceinline__ void blk_carry(Blk<MM>& b, int m, int64_t& top) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  int64_t c = blk_add(b, m, 0);
+#pragma unroll
+  for (int pass = 0; pass < 2; pass++) {
+    int64_t cin = __shfl_up_sync(full, c, 1);
+    top += __shfl_sync(full, c, 31);
+    if (lane == 0) cin = 0;
+    c = blk_add(b, m, cin);
+  }
+  blk_resolve(b, m, (int)c, top);
+}
+
+template <int MM>
+__device__ bool warp_normalize_t(const int64_t* col, int ncols, int drop, int W, int32_t* out) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int m = (ncols + 31) / 32;
+  Blk<MM> b;
+#pragma unroll
+  for (int j = 0; j < MM; j++) {
+    const int c = lane * m + j;
+    b.v[j] = (j < m && c < ncols) ? col[c] : 0;
+  }
+  int64_t top = 0;
+  blk_carry(b, m, top);  // digits in [0, B), signed carry in `top`
+  if (drop) {
+    // + B^drop / 2 == + B/2 at column drop-1, then floor: discard columns < drop
+    int e = 0;
+    if (lane * m <= drop - 1 && drop - 1 < lane * m + m) {
+      Blk<MM> add;
+#pragma unroll
+      for (int j = 0; j < MM; j++) add.v[j] = 0;
+      int64_t cin = 0;
+#pragma unroll
+      for (int j = 0; j < MM; j++) {
         if (j < m) {
-          int64_t t = v[j] + cin;
-          int64_t d = t & kMask;
-          cin = (t - d) >> kRadixBits;
-          v[j] = d;
+          const int64_t t = b.v[j] + cin + ((lane * m + j == drop - 1) ? (kRadix / 2) : 0);
+          const int64_t dgt = t & kMask;
+          cin = (t - dgt) >> kRadixBits;
+          b.v[j] = dgt;
         }
       }
-      c = cin;
+      e = (int)cin;
+    }
+    blk_resolve(b, m, e, top);
+#pragma unroll
+    for (int j = 0; j < MM; j++)
+      if (lane * m + j < drop) b.v[j] = 0;
+  }
+  const bool neg = top < 0;
+  if (neg) {
+    // |R| = -R: complement the kept digits and add one at column `drop`
+    int e = 0;
+#pragma unroll
+    for (int j = 0; j < MM; j++)
+      if (j < m && lane * m + j >= drop) b.v[j] = kMask - b.v[j];
+    top = -top - 1;
+    if (lane * m <= drop && drop < lane * m + m) {
+      int64_t cin = 0;
+#pragma unroll
+      for (int j = 0; j < MM; j++) {
+        if (j < m) {
+          const int64_t t = b.v[j] + cin + ((lane * m + j == drop) ? 1 : 0);
+          const int64_t dgt = t & kMask;
+          cin = (t - dgt) >> kRadixBits;
+          b.v[j] = dgt;
+        }
+      }
+      e = (int)cin;
+    }
+    blk_resolve(b, m, e, top);
+  }
+  bool ovf = top != 0;
+#pragma unroll
+  for (int j = 0; j < MM; j++) {
+    const int c = lane * m + j;
+    if (j < m && c >= drop) {
+      const int d = c - drop;
+      const int32_t dig = (int32_t)b.v[j];
+      if (d < W)
+        out[d] = neg ? -dig : dig;
+      else if (dig)
+        ovf = true;
     }
   }
-  top = __shfl_sync(full, top, 31);
+  for (int d = 32 * m - drop + lane; d < W; d += 32) out[d] = 0;
+  return __any_sync(full, ovf);
 }
 
 __device__ inline void round_to_prec(int32_t* out, int W, int prec_bits, bool& ovf) {
@@ -177,51 +287,21 @@ __device__ inline void round_to_prec(int32_t* out, int W, int prec_bits, bool& o
 }
 
 __device__ inline bool warp_normalize(const int64_t* col, int ncols, int drop, int W, int32_t* out, int2* info,
-                               int round_prec_bits) {
+                                      int round_prec_bits) {
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int m = (ncols + 31) / 32;
-  int64_t v[kMaxLanesDigits];
-#pragma unroll
-  for (int j = 0; j < kMaxLanesDigits; j++) {
-    int c = lane * m + j;
-    v[j] = (j < m && c < ncols) ? col[c] : 0;
-  }
-  int64_t top = 0;
-  warp_carry(v, m, top);  // digits in [0, B), signed carry in `top`
-  if (drop) {
-    // floor((V + B^drop/2) / B^drop): add B/2 at column drop-1, propagate,
-    // then discard the (non-negative) low digits.
-#pragma unroll
-    for (int j = 0; j < kMaxLanesDigits; j++)
-      if (lane * m + j == drop - 1) v[j] += kRadix / 2;
-    warp_carry(v, m, top);
-#pragma unroll
-    for (int j = 0; j < kMaxLanesDigits; j++)
-      if (lane * m + j < drop) v[j] = 0;
-  }
-  const bool neg = top < 0;
-  if (neg) {  // magnitude of a negative result: negate and renormalise
-#pragma unroll
-    for (int j = 0; j < kMaxLanesDigits; j++) v[j] = -v[j];
-    top = -top;
-    warp_carry(v, m, top);
-  }
-  bool ovf = top != 0;
-#pragma unroll
-  for (int j = 0; j < kMaxLanesDigits; j++) {
-    int c = lane * m + j;
-    if (j < m && c >= drop && c < ncols) {
-      int d = c - drop;
-      int32_t dig = (int32_t)v[j];
-      if (d < W)
-        out[d] = neg ? -dig : dig;
-      else if (dig)
-        ovf = true;
-    }
-  }
-  for (int d = ncols - drop + lane; d < W; d += 32) out[d] = 0;
-  ovf = __any_sync(full, ovf);
+  bool ovf;
+  if (m <= 2)
+    ovf = warp_normalize_t<2>(col, ncols, drop, W, out);
+  else if (m <= 4)
+    ovf = warp_normalize_t<4>(col, ncols, drop, W, out);
+  else if (m <= 8)
+    ovf = warp_normalize_t<8>(col, ncols, drop, W, out);
+  else if (m <= 16)
+    ovf = warp_normalize_t<16>(col, ncols, drop, W, out);
+  else
+    ovf = warp_normalize_t<kMaxLanesDigits>(col, ncols, drop, W, out);
   __syncwarp();
   if (round_prec_bits > 0) {
     if (lane == 0) round_to_prec(out, W, round_prec_bits, ovf);
@@ -240,6 +320,5 @@ __device__ inline bool warp_normalize(const int64_t* col, int ncols, int drop, i
   __syncwarp();
   return ovf;
 }
-
 
 }  // namespace mpt

@@ -59,7 +59,10 @@ struct Layout {
   int base[kMaxD], full[kMaxD];  // per variable: first slot, 1 = every index kept
   int ncrow;     // constant rows: cst D, lin D*D, q NT, ctab 1, U D, S NP, cur D
   int ntg;       // exchange targets: NP pair sums + D linear-product sums
-  size_t off_rows, off_rinfo, off_crow, off_cinfo, off_xbuf, off_cols, off_ssum, off_flag, total;
+  int nunits;    // partial-sum units (one writer per (unit, column group))
+  int ngmax;     // column groups per unit
+  size_t off_rows, off_rinfo, off_crow, off_cinfo, off_xbuf, off_cols, off_ssum, off_part, off_pcar, off_utg,
+      off_flag, total;
 };
 
 // rows: a variable that appears as a left factor keeps all N+1 indices; a
@@ -93,6 +96,15 @@ __host__ __device__ inline Layout make_layout(const Params& p, int G) {
   L.off_xbuf = take(sizeof(int64_t) * 2 * (size_t)L.ntg * g.NCX);
   L.off_cols = take(sizeof(int64_t) * (size_t)(L.ntg + p.D) * g.NCX);
   L.off_ssum = take(sizeof(int64_t) * (size_t)p.D * (p.W + 3));
+  const int ns = kThreads / g.NGb;
+  int nu = ns * (p.NP > 0 ? p.NP : 1) + p.D * p.D;
+  if (p.NT > nu) nu = p.NT;
+  if (p.D * kPC > nu) nu = p.D * kPC;
+  L.nunits = nu;
+  L.ngmax = g.NGb > g.NGc ? g.NGb : g.NGc;
+  L.off_part = take(sizeof(uint32_t) * (size_t)nu * g.NCX);
+  L.off_pcar = take(sizeof(int64_t) * (size_t)nu * L.ngmax);
+  L.off_utg = take(sizeof(int) * (size_t)nu);
   L.off_flag = take(sizeof(int) * 8);
   L.total = o;
   return L;
@@ -110,12 +122,30 @@ __device__ __forceinline__ int2 row_info_warp(const int32_t* row, int W) {
   return make_int2(tp >= 0 ? bot : W, tp);
 }
 
-__device__ __forceinline__ void add_cols(int64_t* dst, const Acc& a, int c0, int T, int ncx) {
+// one writer per (unit, group): the folded digits (in [0, B)) of the group's
+// columns and the group's carry into the next group's first column
+__device__ __forceinline__ void store_unit(uint32_t* part, int64_t* pcar, const Acc& a, int grp, int c0, int T) {
 #pragma unroll
-  for (int r = 0; r <= kR; r++) {
+  for (int r = 0; r < kR; r++) {
     const int c = c0 + r - T;
-    if (c >= 0 && c < ncx && a.v[r] != 0) atomicAdd((unsigned long long*)&dst[c], (unsigned long long)a.v[r]);
+    if (c >= 0) part[c] = (uint32_t)a.v[r];
   }
+  pcar[grp] = a.v[kR];
+}
+
+// column sums of target `tg` over its units: digits plus the carries that
+// land on group boundaries (column c0 + kR of group grp)
+__device__ __forceinline__ int64_t unit_sum(const uint32_t* part, const int64_t* pcar, const int* utg, int nunits,
+                                            int ncx, int ngmax, int tg, int c, int T, int gf, int ng) {
+  int64_t s = 0;
+  const int cabs = c + T;
+  const int cg = (cabs % kR == 0) ? cabs / kR - 1 - gf : -1;  // group whose carry lands here
+  for (int u = 0; u < nunits; u++) {
+    if (utg[u] != tg) continue;
+    s += part[(size_t)u * ncx + c];
+    if (cg >= 0 && cg < ng) s += pcar[(size_t)u * ngmax + cg];
+  }
+  return s;
 }
 
 template <int NPT>
@@ -136,6 +166,9 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cluster_kernel(const __gri
   int64_t* xbuf = (int64_t*)(smem + L.off_xbuf);
   int64_t* cols = (int64_t*)(smem + L.off_cols);
   int64_t* ssum = (int64_t*)(smem + L.off_ssum);
+  uint32_t* part = (uint32_t*)(smem + L.off_part);
+  int64_t* pcar = (int64_t*)(smem + L.off_pcar);
+  int* utg = (int*)(smem + L.off_utg);
   int* flag = (int*)(smem + L.off_flag);
   const int rs = L.rs;
   // constant-row indices
@@ -197,13 +230,12 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cluster_kernel(const __gri
       int64_t* xb = xbuf + (size_t)(i & 1) * L.ntg * g.NCX;
       // tau/(i+1) row: issue the loads early, used in phase C
       for (int d = tid; d < p.W; d += kThreads) CROW(CR_CT)[d] = __ldg(p.ctab + (size_t)i * p.RS + d);
-      for (int w = tid; w < L.ntg * g.NCX; w += kThreads) xb[w] = 0;
-      __syncthreads();
       // ================= phase A: Cauchy partial sums for k = rank (mod G)
-      if (p.NP > 0 && rank <= i) {
-        const int nk = (i - rank) / G + 1;
+      {
         const int ns = kThreads / g.NGb;
         const int slot = tid / g.NGb, grp = tid - slot * g.NGb;
+        const int nu_a = ns * p.NP;
+        for (int u = tid; u < nu_a + nlin; u += kThreads) utg[u] = u < nu_a ? u % p.NP : p.NP + (u - nu_a) / p.D;
         if (slot < ns) {
           const int c0 = kR * (g.gfb + grp);
           Acc acc[NPT];
@@ -213,6 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cluster_kernel(const __gri
             acc_zero(acc[q]);
             cnt[q] = 0;
           }
+          const int nk = rank <= i ? (i - rank) / G + 1 : 0;
           for (int kk = slot; kk < nk; kk += ns) {
             const int k = rank + kk * G;
 #pragma unroll
@@ -228,24 +261,34 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cluster_kernel(const __gri
           for (int q = 0; q < NPT; q++) {
             if (q < p.NP) {
               acc_fold(acc[q], c0, g.Tb);
-              add_cols(xb + (size_t)q * g.NCX, acc[q], c0, g.Tb, g.NCX);
+              const int u = slot * p.NP + q;
+              store_unit(part + (size_t)u * g.NCX, pcar + (size_t)u * L.ngmax, acc[q], grp, c0, g.Tb);
             }
           }
         }
-      }
-      // non-small-integer linear terms: item e -> CTA e % G
-      for (int e = tid; e < nlin * g.NGb; e += kThreads) {
-        const int it = e / g.NGb, grp = e - it * g.NGb;
-        if (p.lin_small[it] || (it % G) != rank) continue;
-        const int m = it / p.D, j = it - m * p.D;
-        if (cinfo[CR_LIN + it].y < 0) continue;
-        const int c0 = kR * (g.gfb + grp);
-        Acc acc;
-        acc_zero(acc);
-        int cnt = 0;
-        mac_group(acc, cnt, CROW(CR_LIN + it), cinfo[CR_LIN + it], CROW(CR_CUR + j), cinfo[CR_CUR + j], c0, g.Tb, mc);
-        acc_fold(acc, c0, g.Tb);
-        add_cols(xb + (size_t)(p.NP + m) * g.NCX, acc, c0, g.Tb, g.NCX);
+        // linear terms with non-small-integer coefficients: item it -> CTA it % G
+        for (int e = tid; e < nlin * g.NGb; e += kThreads) {
+          const int it = e / g.NGb, grp2 = e - it * g.NGb;
+          const int m = it / p.D, j = it - m * p.D;
+          const int c0 = kR * (g.gfb + grp2);
+          Acc acc;
+          acc_zero(acc);
+          if (!p.lin_small[it] && (it % G) == rank && cinfo[CR_LIN + it].y >= 0) {
+            int cnt = 0;
+            mac_group(acc, cnt, CROW(CR_LIN + it), cinfo[CR_LIN + it], CROW(CR_CUR + j), cinfo[CR_CUR + j], c0, g.Tb,
+                      mc);
+            acc_fold(acc, c0, g.Tb);
+          }
+          const int u = nu_a + it;
+          store_unit(part + (size_t)u * g.NCX, pcar + (size_t)u * L.ngmax, acc, grp2, c0, g.Tb);
+        }
+        __syncthreads();
+        // this CTA's exchange buffer: per target column sums over its units
+        for (int w = tid; w < L.ntg * g.ncolb; w += kThreads) {
+          const int tg = w / g.ncolb, c = w - tg * g.ncolb;
+          xb[(size_t)tg * g.NCX + c] =
+              unit_sum(part, pcar, utg, nu_a + nlin, g.NCX, L.ngmax, tg, c, g.Tb, g.gfb, g.NGb);
+        }
       }
       __syncthreads();
       // ================= exchange: one cluster barrier, then DSMEM gather
@@ -285,20 +328,29 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cluster_kernel(const __gri
         ucol[(size_t)m * g.NCX + c] = s;
       }
       __syncthreads();
-      // non-integer q terms: tprod(q_t, S_p)
-      for (int e = tid; e < p.NT * g.NGb; e += kThreads) {
-        const int t = e / g.NGb, grp = e - t * g.NGb;
-        if (p.tq_small[t]) continue;
-        const int c0 = kR * (g.gfb + grp);
-        Acc acc;
-        acc_zero(acc);
-        int cnt = 0;
-        mac_group(acc, cnt, CROW(CR_Q + t), cinfo[CR_Q + t], CROW(CR_S + p.tpair[t]), cinfo[CR_S + p.tpair[t]], c0,
-                  g.Tb, mc);
-        acc_fold(acc, c0, g.Tb);
-        add_cols(ucol + (size_t)p.teq[t] * g.NCX, acc, c0, g.Tb, g.NCX);
+      // non-integer q terms: tprod(q_t, S_p) (general systems only)
+      if (p.NP > 0 && !p.all_q_small) {
+        for (int u = tid; u < p.NT; u += kThreads) utg[u] = p.teq[u];
+        for (int e = tid; e < p.NT * g.NGb; e += kThreads) {
+          const int t = e / g.NGb, grp = e - t * g.NGb;
+          const int c0 = kR * (g.gfb + grp);
+          Acc acc;
+          acc_zero(acc);
+          if (!p.tq_small[t]) {
+            int cnt = 0;
+            mac_group(acc, cnt, CROW(CR_Q + t), cinfo[CR_Q + t], CROW(CR_S + p.tpair[t]), cinfo[CR_S + p.tpair[t]],
+                      c0, g.Tb, mc);
+            acc_fold(acc, c0, g.Tb);
+          }
+          store_unit(part + (size_t)t * g.NCX, pcar + (size_t)t * L.ngmax, acc, grp, c0, g.Tb);
+        }
+        __syncthreads();
+        for (int w = tid; w < p.D * g.ncolb; w += kThreads) {
+          const int m = w / g.ncolb, c = w - m * g.ncolb;
+          ucol[(size_t)m * g.NCX + c] += unit_sum(part, pcar, utg, p.NT, g.NCX, L.ngmax, m, c, g.Tb, g.gfb, g.NGb);
+        }
+        __syncthreads();
       }
-      __syncthreads();
       for (int m = warp; m < p.D; m += nwarps) {
         if (warp_normalize(ucol + (size_t)m * g.NCX, g.ncolb, 2, p.W, CROW(CR_U + m), &cinfo[CR_U + m], 0) && lane == 0)
           flag[0] = 1;
@@ -309,28 +361,35 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cluster_kernel(const __gri
       }
       __syncthreads();
       // ================= phase C: coef[m][i+1] = rnd(U_m (x) tau/(i+1))
-      for (int w = tid; w < p.D * g.NCX; w += kThreads) ucol[w] = 0;
-      __syncthreads();
+      for (int u = tid; u < p.D * kPC; u += kThreads) utg[u] = u / kPC;
       for (int e = tid; e < p.D * g.NGc * kPC; e += kThreads) {
         const int m = e / (g.NGc * kPC), rem = e - m * g.NGc * kPC, grp = rem / kPC, pc = rem - grp * kPC;
         const int c0 = kR * (g.gfc + grp);
         int2 ia = cinfo[CR_U + m];
         const int2 ib = cinfo[CR_CT];
-        // split the p range of this group into kPC chunks of whole kR blocks
-        const int plo = max(ia.x, c0 - ib.y), phi = min(ia.y, c0 + kR - 1 - ib.x);
-        if (plo > phi) continue;
-        const int b0 = plo / kR, nb = phi / kR - b0 + 1;
-        const int per = (nb + kPC - 1) / kPC;
-        const int blo = b0 + pc * per, bhi = min(b0 + nb, blo + per) - 1;
-        if (blo > bhi) continue;
-        ia.x = max(ia.x, blo * kR);
-        ia.y = min(ia.y, bhi * kR + kR - 1);
         Acc acc;
         acc_zero(acc);
-        int cnt = 0;
-        mac_group(acc, cnt, CROW(CR_U + m), ia, CROW(CR_CT), ib, c0, g.Tc, mc);
-        acc_fold(acc, c0, g.Tc);
-        add_cols(ucol + (size_t)m * g.NCX, acc, c0, g.Tc, g.NCX);
+        // split the p range of this group into kPC chunks of whole kR blocks
+        const int plo = max(ia.x, c0 - ib.y), phi = min(ia.y, c0 + kR - 1 - ib.x);
+        if (plo <= phi) {
+          const int b0 = plo / kR, nb = phi / kR - b0 + 1;
+          const int per = (nb + kPC - 1) / kPC;
+          const int blo = b0 + pc * per, bhi = min(b0 + nb, blo + per) - 1;
+          if (blo <= bhi) {
+            ia.x = max(ia.x, blo * kR);
+            ia.y = min(ia.y, bhi * kR + kR - 1);
+            int cnt = 0;
+            mac_group(acc, cnt, CROW(CR_U + m), ia, CROW(CR_CT), ib, c0, g.Tc, mc);
+            acc_fold(acc, c0, g.Tc);
+          }
+        }
+        const int u = m * kPC + pc;
+        store_unit(part + (size_t)u * g.NCX, pcar + (size_t)u * L.ngmax, acc, grp, c0, g.Tc);
+      }
+      __syncthreads();
+      for (int w = tid; w < p.D * g.ncolc; w += kThreads) {
+        const int m = w / g.ncolc, c = w - m * g.ncolc;
+        ucol[(size_t)m * g.NCX + c] = unit_sum(part, pcar, utg, p.D * kPC, g.NCX, L.ngmax, m, c, g.Tc, g.gfc, g.NGc);
       }
       __syncthreads();
       for (int m = warp; m < p.D; m += nwarps) {
