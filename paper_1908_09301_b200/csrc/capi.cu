@@ -21,6 +21,7 @@ int max_cluster_size(const Params& p, size_t smem, int want);
 }  // namespace mpt
 
 static thread_local std::string g_err;
+static long long* g_dbg = nullptr;  // MPT_DEBUG dump buffer (development only)
 
 static int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -334,8 +335,16 @@ static int ensure_rec(mpt_plan* pl, size_t slots) {
   return MPT_OK;
 }
 
-static int launch(mpt_plan* pl, int n_steps, int start_step, int stride, cudaStream_t stream) {
+static int launch(mpt_plan* pl, int n_steps, int start_step, int stride, cudaStream_t stream, int write_coef = 0) {
   mpt::Params p = pl->p;
+  p.write_coef = write_coef;
+  if (getenv("MPT_DEBUG")) {
+    if (!g_dbg) cudaMalloc((void**)&g_dbg, 8 * 4096);
+    cudaMemset(g_dbg, 0, 8 * 4096);
+    p.dbg = g_dbg;
+  } else {
+    p.dbg = nullptr;
+  }
   p.n_steps = n_steps;
   p.start_step = start_step;
   p.stride = stride;
@@ -418,7 +427,7 @@ int mpt_compute_jet(mpt_plan* pl, const int32_t* state, int32_t* coef, int32_t* 
   int rc;
   if ((rc = ensure_rec(pl, 2))) return rc;
   if ((rc = mpt_state_upload(pl, state))) return rc;
-  if ((rc = launch(pl, 1, 0, 2, 0))) return rc;
+  if ((rc = launch(pl, 1, 0, 2, 0, 1))) return rc;
   if ((rc = finish(pl, 0, status))) return rc;
   const mpt::Params& p = pl->p;
   if ((rc = download_rows(coef, pl->d_coef, (size_t)p.n_traj * p.D * (p.N + 1), p.W, p.RS))) return rc;
@@ -440,6 +449,12 @@ int mpt_step(mpt_plan* pl, const int32_t* state, int32_t* state_out, int32_t* st
   if (status)
     for (int t = 0; t < pl->p.n_traj; t++)
       if (status[t]) return fail(MPT_ERANGE, "fixed-point range exceeded on the device");
+  return MPT_OK;
+}
+
+int mpt_debug_read(long long* host, int n) {
+  if (!g_dbg) return MPT_EINVAL;
+  cudaMemcpy(host, g_dbg, 8 * (size_t)n, cudaMemcpyDeviceToHost);
   return MPT_OK;
 }
 

@@ -59,6 +59,8 @@ struct Params {
   int kc;               // k values staged per chunk
   int nthreads;
   unsigned long long* counters;  // optional: [0] useful limb-MACs, [1] executed limb-MACs
+  int write_coef;                // cluster kernel: also store every coefficient row to `coef`
+  long long* dbg;                // debug dump (nullptr in production)
 };
 
 }  // namespace mpt

@@ -173,7 +173,7 @@ __device__ __forceinline__ void blk_carry(Blk<MM>& b, int m, int64_t& top) {
 }
 
 template <int MM>
-__device__ bool warp_normalize_t(const int64_t* col, int ncols, int drop, int W, int32_t* out) {
+__device__ __forceinline__ bool warp_normalize_t(const int64_t* col, int ncols, int drop, int W, int32_t* out) {
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int m = (ncols + 31) / 32;
@@ -189,9 +189,6 @@ __device__ bool warp_normalize_t(const int64_t* col, int ncols, int drop, int W,
     // + B^drop / 2 == + B/2 at column drop-1, then floor: discard columns < drop
     int e = 0;
     if (lane * m <= drop - 1 && drop - 1 < lane * m + m) {
-      Blk<MM> add;
-#pragma unroll
-      for (int j = 0; j < MM; j++) add.v[j] = 0;
       int64_t cin = 0;
 #pragma unroll
       for (int j = 0; j < MM; j++) {
@@ -286,7 +283,7 @@ __device__ inline void round_to_prec(int32_t* out, int W, int prec_bits, bool& o
   if (cin) ovf = true;
 }
 
-__device__ inline bool warp_normalize(const int64_t* col, int ncols, int drop, int W, int32_t* out, int2* info,
+__device__ __forceinline__ bool warp_normalize(const int64_t* col, int ncols, int drop, int W, int32_t* out, int2* info,
                                       int round_prec_bits) {
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;

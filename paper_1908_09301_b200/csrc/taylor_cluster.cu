@@ -139,11 +139,13 @@ __device__ __forceinline__ int64_t unit_sum(const uint32_t* part, const int64_t*
                                             int ncx, int ngmax, int tg, int c, int T, int gf, int ng) {
   int64_t s = 0;
   const int cabs = c + T;
+  const int own = cabs / kR - gf;                             // group that stores this column
   const int cg = (cabs % kR == 0) ? cabs / kR - 1 - gf : -1;  // group whose carry lands here
+  const bool has_digit = own >= 0 && own < ng, has_carry = cg >= 0 && cg < ng;
   for (int u = 0; u < nunits; u++) {
     if (utg[u] != tg) continue;
-    s += part[(size_t)u * ncx + c];
-    if (cg >= 0 && cg < ng) s += pcar[(size_t)u * ngmax + cg];
+    if (has_digit) s += part[(size_t)u * ncx + c];
+    if (has_carry) s += pcar[(size_t)u * ngmax + cg];
   }
   return s;
 }
@@ -224,6 +226,10 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cluster_kernel(const __gri
         if (has_row(m, 0)) rinfo[SLOT(m, 0)] = inf;
       }
     }
+    if (p.write_coef && rank == 0)
+      for (int m = 0; m < p.D; m++)
+        for (int d = tid; d < p.W; d += kThreads)
+          p.coef[(((size_t)traj * p.D + m) * (p.N + 1)) * p.RS + d] = CROW(CR_CUR + m)[d];
     __syncthreads();
 
     for (int i = 0; i < p.N; i++) {
@@ -392,6 +398,20 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cluster_kernel(const __gri
         ucol[(size_t)m * g.NCX + c] = unit_sum(part, pcar, utg, p.D * kPC, g.NCX, L.ngmax, m, c, g.Tc, g.gfc, g.NGc);
       }
       __syncthreads();
+      if (p.dbg && i == 0 && n == p.start_step + 1 && rank == 0) {
+        for (int c = tid; c < g.ncolc; c += kThreads) p.dbg[c] = ucol[c];
+        for (int d = tid; d < p.W; d += kThreads) p.dbg[100 + d] = CROW(CR_U)[d];
+        for (int d = tid; d < p.W; d += kThreads) p.dbg[200 + d] = CROW(CR_CT)[d];
+        if (tid == 0) {
+          p.dbg[300] = cinfo[CR_U].x; p.dbg[301] = cinfo[CR_U].y; p.dbg[302] = cinfo[CR_CT].x; p.dbg[303] = cinfo[CR_CT].y;
+          p.dbg[304] = g.ncolc; p.dbg[305] = g.Tc; p.dbg[306] = g.NGc; p.dbg[307] = g.gfc;
+        }
+        for (int u = 0; u < p.D * kPC; u++)
+          for (int c = tid; c < g.NCX; c += kThreads) p.dbg[400 + u * 64 + c] = part[(size_t)u * g.NCX + c];
+        for (int u = 0; u < p.D * kPC; u++)
+          for (int c = tid; c < L.ngmax; c += kThreads) p.dbg[1400 + u * 8 + c] = pcar[(size_t)u * L.ngmax + c];
+      }
+      __syncthreads();
       for (int m = warp; m < p.D; m += nwarps) {
         if (warp_normalize(ucol + (size_t)m * g.NCX, g.ncolc, 2, p.W, CROW(CR_CUR + m), &cinfo[CR_CUR + m], 0) &&
             lane == 0)
@@ -407,6 +427,10 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cluster_kernel(const __gri
           if (keep) ROW(m, i + 1)[d] = cur[d];
         }
         if (keep && tid == 0) rinfo[SLOT(m, i + 1)] = cinfo[CR_CUR + m];
+        if (p.write_coef && rank == 0) {
+          int32_t* dst = p.coef + (((size_t)traj * p.D + m) * (p.N + 1) + i + 1) * p.RS;
+          for (int d = tid; d < p.W; d += kThreads) dst[d] = cur[d];
+        }
       }
       __syncthreads();
     }

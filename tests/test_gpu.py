@@ -56,7 +56,11 @@ def test_every_kernel_bit_exact_vs_model(gpu, kernel, cluster, P, N, steps):
     ctx, system, fmt, tables = lorenz_tables(P, N)
     st = fmt.to_digits([M.mp_from_decimal(t, ctx) for t in CANON_INIT])
     with DevicePlan(tables, fmt, N, 1) as plan:
-        plan.configure(kernel, cluster)
+        try:
+            plan.configure(kernel, cluster)
+        except Exception as exc:  # rows do not fit this cluster size's shared memory
+            assert "shared memory" in str(exc)
+            pytest.skip(str(exc))
         info = plan.info()
         assert info["kernel"] == kernel
         s_gpu, r_gpu, status = plan.integrate(st, steps, 0, 1)
