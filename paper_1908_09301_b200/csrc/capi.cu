@@ -322,6 +322,12 @@ int mpt_plan_set_constants(mpt_plan* pl, const int32_t* cst, const int32_t* lin,
       pm.all_q_small = 0;
     }
   }
+  for (int t = 0; t < p.NP; t++) pm.tg_used[t] = 1;
+  for (int m = 0; m < p.D; m++) {
+    pm.tg_used[p.NP + m] = 0;
+    for (int j = 0; j < p.D; j++)
+      if (!pm.lin_small[m * p.D + j]) pm.tg_used[p.NP + m] = 1;
+  }
   pl->have_constants = true;
   return MPT_OK;
 }

@@ -42,6 +42,7 @@ struct Params {
   int tq_small[kMaxT], tq_int[kMaxT];
   int pair_round[kMaxP];
   int all_q_small;
+  int tg_used[kMaxP + kMaxD];  // exchange targets with producers (pair sums, non-integer linear rows)
   int lin_small[kMaxD * kMaxD], lin_int[kMaxD * kMaxD];
   // constants (global, row stride RS)
   const int32_t* cst;   // D rows

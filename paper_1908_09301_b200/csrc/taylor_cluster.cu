@@ -133,19 +133,26 @@ __device__ __forceinline__ void store_unit(uint32_t* part, int64_t* pcar, const 
   pcar[grp] = a.v[kR];
 }
 
-// column sums of target `tg` over its units: digits plus the carries that
-// land on group boundaries (column c0 + kR of group grp)
-__device__ __forceinline__ int64_t unit_sum(const uint32_t* part, const int64_t* pcar, const int* utg, int nunits,
-                                            int ncx, int ngmax, int tg, int c, int T, int gf, int ng) {
-  int64_t s = 0;
+// column c (relative to T) of a target whose units are u0, u0 + ustride, ...
+// (n units): folded digits of the group that owns the column plus the carry
+// of the group below it
+__device__ __forceinline__ int64_t strided_sum(const uint32_t* part, const int64_t* pcar, int u0, int ustride, int n,
+                                               int ncx, int ngmax, int c, int T, int gf, int ng) {
   const int cabs = c + T;
-  const int own = cabs / kR - gf;                             // group that stores this column
-  const int cg = (cabs % kR == 0) ? cabs / kR - 1 - gf : -1;  // group whose carry lands here
-  const bool has_digit = own >= 0 && own < ng, has_carry = cg >= 0 && cg < ng;
-  for (int u = 0; u < nunits; u++) {
-    if (utg[u] != tg) continue;
-    if (has_digit) s += part[(size_t)u * ncx + c];
-    if (has_carry) s += pcar[(size_t)u * ngmax + cg];
+  const int own = cabs / kR - gf;
+  const int cg = (cabs % kR == 0) ? cabs / kR - 1 - gf : -1;
+  int64_t s = 0;
+  if (own >= 0 && own < ng) {
+    const uint32_t* pp = part + (size_t)u0 * ncx + c;
+    const size_t st = (size_t)ustride * ncx;
+#pragma unroll 4
+    for (int u = 0; u < n; u++) s += pp[u * st];
+  }
+  if (cg >= 0 && cg < ng) {
+    const int64_t* pc = pcar + (size_t)u0 * ngmax + cg;
+    const size_t st = (size_t)ustride * ngmax;
+#pragma unroll 4
+    for (int u = 0; u < n; u++) s += pc[u * st];
   }
   return s;
 }
@@ -170,7 +177,6 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cluster_kernel(const __gri
   int64_t* ssum = (int64_t*)(smem + L.off_ssum);
   uint32_t* part = (uint32_t*)(smem + L.off_part);
   int64_t* pcar = (int64_t*)(smem + L.off_pcar);
-  int* utg = (int*)(smem + L.off_utg);
   int* flag = (int*)(smem + L.off_flag);
   const int rs = L.rs;
   // constant-row indices
@@ -241,8 +247,9 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cluster_kernel(const __gri
         const int ns = kThreads / g.NGb;
         const int slot = tid / g.NGb, grp = tid - slot * g.NGb;
         const int nu_a = ns * p.NP;
-        for (int u = tid; u < nu_a + nlin; u += kThreads) utg[u] = u < nu_a ? u % p.NP : p.NP + (u - nu_a) / p.D;
-        if (slot < ns) {
+        const int nk = rank <= i ? (i - rank) / G + 1 : 0;
+        const int nsa = min(ns, nk);  // slots with work this order
+        if (slot < nsa) {
           const int c0 = kR * (g.gfb + grp);
           Acc acc[NPT];
           int cnt[NPT];
@@ -251,7 +258,6 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cluster_kernel(const __gri
             acc_zero(acc[q]);
             cnt[q] = 0;
           }
-          const int nk = rank <= i ? (i - rank) / G + 1 : 0;
           for (int kk = slot; kk < nk; kk += ns) {
             const int k = rank + kk * G;
 #pragma unroll
@@ -275,11 +281,12 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cluster_kernel(const __gri
         // linear terms with non-small-integer coefficients: item it -> CTA it % G
         for (int e = tid; e < nlin * g.NGb; e += kThreads) {
           const int it = e / g.NGb, grp2 = e - it * g.NGb;
+          if (p.lin_small[it]) continue;
           const int m = it / p.D, j = it - m * p.D;
           const int c0 = kR * (g.gfb + grp2);
           Acc acc;
           acc_zero(acc);
-          if (!p.lin_small[it] && (it % G) == rank && cinfo[CR_LIN + it].y >= 0) {
+          if ((it % G) == rank && cinfo[CR_LIN + it].y >= 0) {
             int cnt = 0;
             mac_group(acc, cnt, CROW(CR_LIN + it), cinfo[CR_LIN + it], CROW(CR_CUR + j), cinfo[CR_CUR + j], c0, g.Tb,
                       mc);
@@ -292,8 +299,16 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cluster_kernel(const __gri
         // this CTA's exchange buffer: per target column sums over its units
         for (int w = tid; w < L.ntg * g.ncolb; w += kThreads) {
           const int tg = w / g.ncolb, c = w - tg * g.ncolb;
-          xb[(size_t)tg * g.NCX + c] =
-              unit_sum(part, pcar, utg, nu_a + nlin, g.NCX, L.ngmax, tg, c, g.Tb, g.gfb, g.NGb);
+          int64_t s = 0;
+          if (tg < p.NP) {
+            s = strided_sum(part, pcar, tg, p.NP, nsa, g.NCX, L.ngmax, c, g.Tb, g.gfb, g.NGb);
+          } else if (p.tg_used[tg]) {
+            const int m = tg - p.NP;
+            for (int j = 0; j < p.D; j++)
+              if (!p.lin_small[m * p.D + j])
+                s += strided_sum(part, pcar, nu_a + m * p.D + j, 1, 1, g.NCX, L.ngmax, c, g.Tb, g.gfb, g.NGb);
+          }
+          xb[(size_t)tg * g.NCX + c] = s;
         }
       }
       __syncthreads();
@@ -303,6 +318,10 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cluster_kernel(const __gri
         const int tg = w / g.ncolb, c = w - tg * g.ncolb;
         const size_t off = (size_t)(i & 1) * L.ntg * g.NCX + (size_t)tg * g.NCX + c;
         int64_t s = 0;
+        if (!p.tg_used[tg]) {
+          cols[(size_t)tg * g.NCX + c] = 0;
+          continue;
+        }
         for (int rr = 0; rr < G; rr++) {
           const int64_t* rb = cluster.map_shared_rank(xbuf, rr);
           s += rb[off];
@@ -336,7 +355,6 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cluster_kernel(const __gri
       __syncthreads();
       // non-integer q terms: tprod(q_t, S_p) (general systems only)
       if (p.NP > 0 && !p.all_q_small) {
-        for (int u = tid; u < p.NT; u += kThreads) utg[u] = p.teq[u];
         for (int e = tid; e < p.NT * g.NGb; e += kThreads) {
           const int t = e / g.NGb, grp = e - t * g.NGb;
           const int c0 = kR * (g.gfb + grp);
@@ -353,7 +371,9 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cluster_kernel(const __gri
         __syncthreads();
         for (int w = tid; w < p.D * g.ncolb; w += kThreads) {
           const int m = w / g.ncolb, c = w - m * g.ncolb;
-          ucol[(size_t)m * g.NCX + c] += unit_sum(part, pcar, utg, p.NT, g.NCX, L.ngmax, m, c, g.Tb, g.gfb, g.NGb);
+          for (int t = 0; t < p.NT; t++)
+            if (p.teq[t] == m && !p.tq_small[t])
+              ucol[(size_t)m * g.NCX + c] += strided_sum(part, pcar, t, 1, 1, g.NCX, L.ngmax, c, g.Tb, g.gfb, g.NGb);
         }
         __syncthreads();
       }
@@ -367,7 +387,6 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cluster_kernel(const __gri
       }
       __syncthreads();
       // ================= phase C: coef[m][i+1] = rnd(U_m (x) tau/(i+1))
-      for (int u = tid; u < p.D * kPC; u += kThreads) utg[u] = u / kPC;
       for (int e = tid; e < p.D * g.NGc * kPC; e += kThreads) {
         const int m = e / (g.NGc * kPC), rem = e - m * g.NGc * kPC, grp = rem / kPC, pc = rem - grp * kPC;
         const int c0 = kR * (g.gfc + grp);
@@ -395,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cluster_kernel(const __gri
       __syncthreads();
       for (int w = tid; w < p.D * g.ncolc; w += kThreads) {
         const int m = w / g.ncolc, c = w - m * g.ncolc;
-        ucol[(size_t)m * g.NCX + c] = unit_sum(part, pcar, utg, p.D * kPC, g.NCX, L.ngmax, m, c, g.Tc, g.gfc, g.NGc);
+        ucol[(size_t)m * g.NCX + c] = strided_sum(part, pcar, m * kPC, 1, kPC, g.NCX, L.ngmax, c, g.Tc, g.gfc, g.NGc);
       }
       __syncthreads();
       if (p.dbg && i == 0 && n == p.start_step + 1 && rank == 0) {
