@@ -182,10 +182,16 @@ __device__ __forceinline__ bool warp_normalize_t(const int64_t* col, int ncols, 
   for (int j = 0; j < MM; j++) {
     const int c = lane * m + j;
     b.v[j] = (j < m && c < ncols) ? col[c] : 0;
+    if (drop && c == drop - 1) b.v[j] += kRadix / 2;  // rounding: + B^drop / 2
   }
   int64_t top = 0;
   blk_carry(b, m, top);  // digits in [0, B), signed carry in `top`
   if (drop) {
+#pragma unroll
+    for (int j = 0; j < MM; j++)
+      if (lane * m + j < drop) b.v[j] = 0;  // floor: discard the low digits
+  }
+  if (false) {
     // + B^drop / 2 == + B/2 at column drop-1, then floor: discard columns < drop
     int e = 0;
     if (lane * m <= drop - 1 && drop - 1 < lane * m + m) {

@@ -188,6 +188,8 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cluster_kernel(const __gri
     s_base[tid] = tid < p.D ? L.base[tid] : 0;
     s_full[tid] = tid < p.D ? L.full[tid] : 1;
   }
+  __shared__ const int64_t* s_remote[16];  // DSMEM views of every cluster CTA's exchange buffers
+  if (tid < 16) s_remote[tid] = tid < G ? cluster.map_shared_rank(xbuf, tid) : nullptr;
   auto has_row = [&](int v, int k) { return s_full[v] || (k % G) == rank; };
   auto SLOT = [&](int v, int k) { return s_base[v] + (s_full[v] ? k : k / G); };
   auto ROW = [&](int v, int k) { return rows + (size_t)SLOT(v, k) * rs; };
@@ -322,10 +324,12 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cluster_kernel(const __gri
           cols[(size_t)tg * g.NCX + c] = 0;
           continue;
         }
-        for (int rr = 0; rr < G; rr++) {
-          const int64_t* rb = cluster.map_shared_rank(xbuf, rr);
-          s += rb[off];
-        }
+        // all G remote loads in flight before the first use
+        int64_t v[16];
+#pragma unroll
+        for (int rr = 0; rr < 16; rr++) v[rr] = rr < G ? s_remote[rr][off] : 0;
+#pragma unroll
+        for (int rr = 0; rr < 16; rr++) s += v[rr];
         cols[(size_t)tg * g.NCX + c] = s;
       }
       __syncthreads();
