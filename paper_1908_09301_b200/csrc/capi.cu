@@ -221,7 +221,7 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
     const char* ek = getenv("MPT_KERNEL");
     const char* ec = getenv("MPT_CLUSTER");
     int kernel = ek ? (strcmp(ek, "team") == 0 ? 1 : strcmp(ek, "cluster") == 0 ? 2 : 0) : 0;
-    int want = ec ? atoi(ec) : (n_traj == 1 ? 8 : 1);
+    int want = ec ? atoi(ec) : (n_traj == 1 ? 16 : 1);
     int rc = choose_kernel(pl, kernel, want < 1 ? 1 : want);
     if (rc) {
       mpt_plan_destroy(pl);

@@ -421,20 +421,6 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cluster_kernel(const __gri
         ucol[(size_t)m * g.NCX + c] = strided_sum(part, pcar, m * kPC, 1, kPC, g.NCX, L.ngmax, c, g.Tc, g.gfc, g.NGc);
       }
       __syncthreads();
-      if (p.dbg && i == 0 && n == p.start_step + 1 && rank == 0) {
-        for (int c = tid; c < g.ncolc; c += kThreads) p.dbg[c] = ucol[c];
-        for (int d = tid; d < p.W; d += kThreads) p.dbg[100 + d] = CROW(CR_U)[d];
-        for (int d = tid; d < p.W; d += kThreads) p.dbg[200 + d] = CROW(CR_CT)[d];
-        if (tid == 0) {
-          p.dbg[300] = cinfo[CR_U].x; p.dbg[301] = cinfo[CR_U].y; p.dbg[302] = cinfo[CR_CT].x; p.dbg[303] = cinfo[CR_CT].y;
-          p.dbg[304] = g.ncolc; p.dbg[305] = g.Tc; p.dbg[306] = g.NGc; p.dbg[307] = g.gfc;
-        }
-        for (int u = 0; u < p.D * kPC; u++)
-          for (int c = tid; c < g.NCX; c += kThreads) p.dbg[400 + u * 64 + c] = part[(size_t)u * g.NCX + c];
-        for (int u = 0; u < p.D * kPC; u++)
-          for (int c = tid; c < L.ngmax; c += kThreads) p.dbg[1400 + u * 8 + c] = pcar[(size_t)u * L.ngmax + c];
-      }
-      __syncthreads();
       for (int m = warp; m < p.D; m += nwarps) {
         if (warp_normalize(ucol + (size_t)m * g.NCX, g.ncolc, 2, p.W, CROW(CR_CUR + m), &cinfo[CR_CUR + m], 0) &&
             lane == 0)
