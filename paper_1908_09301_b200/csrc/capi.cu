@@ -18,6 +18,10 @@ cudaError_t launch_imad_probe(int blocks, int threads, int iters, long long* out
 size_t cluster_smem_bytes(const Params& p, int G);
 cudaError_t launch_cluster_kernel(const Params& p, int G, size_t smem, cudaStream_t stream);
 int max_cluster_size(const Params& p, size_t smem, int want);
+size_t pipe_smem_bytes(const Params& p, int G);
+bool pipe_supported(const Params& p);
+cudaError_t launch_pipe_kernel(const Params& p, int G, size_t smem, cudaStream_t stream);
+int pipe_max_cluster(const Params& p, size_t smem, int want);
 }  // namespace mpt
 
 static thread_local std::string g_err;
@@ -49,22 +53,45 @@ struct mpt_plan {
   bool have_constants = false;
   unsigned long long* d_counters = nullptr;
   bool counting = false;
-  int kernel = 0;    // 1 = team kernel (rows in HBM/L2), 2 = cluster kernel (rows in smem)
+  int kernel = 0;    // 1 = team kernel (rows in HBM/L2), 2 = cluster kernel (rows in smem), 3 = pipeline
   int cluster = 1;   // CTAs per trajectory for the cluster kernel
   size_t smem_cluster = 0;
   int optin = 0;
+  int requested_kernel = 0, requested_cluster = 1;
 };
 
 // choose the kernel: the smem-resident cluster kernel when the rows fit,
 // one cluster of `want` CTAs per trajectory (clamped to what co-schedules)
 static int choose_kernel(mpt_plan* pl, int kernel, int want) {
   mpt::Params& p = pl->p;
+  pl->requested_kernel = kernel;
+  pl->requested_cluster = want;
   if (kernel == 1) {
     pl->kernel = 1;
     pl->cluster = 1;
     return MPT_OK;
   }
   const int tries[] = {16, 8, 4, 2, 1};
+  // the pipelined kernel needs the constants (integer bilinear coefficients)
+  if ((kernel == 0 || kernel == 3) && pl->have_constants && mpt::pipe_supported(p)) {
+    for (int G : tries) {
+      if (G > want) continue;
+      size_t s = mpt::pipe_smem_bytes(p, G);
+      if (s > (size_t)pl->optin) continue;
+      if (G > 1 && mpt::pipe_max_cluster(p, s, G) < 1) continue;
+      pl->kernel = 3;
+      pl->cluster = G;
+      pl->smem_cluster = s;
+      return MPT_OK;
+    }
+  }
+  if (kernel == 3) {
+    if (!pl->have_constants) {  // decided again once the constants are known
+      pl->kernel = 0;
+      return MPT_OK;
+    }
+    return fail(MPT_EUNSUP, "the pipelined kernel does not support this system/precision");
+  }
   for (int G : tries) {
     if (G > want) continue;
     size_t s = mpt::cluster_smem_bytes(p, G);
@@ -220,7 +247,7 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
   {
     const char* ek = getenv("MPT_KERNEL");
     const char* ec = getenv("MPT_CLUSTER");
-    int kernel = ek ? (strcmp(ek, "team") == 0 ? 1 : strcmp(ek, "cluster") == 0 ? 2 : 0) : 0;
+    int kernel = ek ? (strcmp(ek, "team") == 0 ? 1 : strcmp(ek, "cluster") == 0 ? 2 : strcmp(ek, "pipe") == 0 ? 3 : 0) : 0;
     int want = ec ? atoi(ec) : (n_traj == 1 ? 16 : 1);
     int rc = choose_kernel(pl, kernel, want < 1 ? 1 : want);
     if (rc) {
@@ -266,7 +293,7 @@ int mpt_plan_width(const mpt_plan* pl) { return pl ? pl->W : MPT_EINVAL; }
 
 int mpt_plan_info(const mpt_plan* pl, int* smem_bytes, int* k_chunk, int* threads) {
   if (!pl) return MPT_EINVAL;
-  if (smem_bytes) *smem_bytes = (int)(pl->kernel == 2 ? pl->smem_cluster : pl->smem);
+  if (smem_bytes) *smem_bytes = (int)(pl->kernel >= 2 ? pl->smem_cluster : pl->smem);
   if (k_chunk) *k_chunk = pl->p.kc;
   if (threads) *threads = pl->p.nthreads;
   return MPT_OK;
@@ -323,13 +350,13 @@ int mpt_plan_set_constants(mpt_plan* pl, const int32_t* cst, const int32_t* lin,
     }
   }
   for (int t = 0; t < p.NP; t++) pm.tg_used[t] = 1;
+  pl->have_constants = true;
   for (int m = 0; m < p.D; m++) {
     pm.tg_used[p.NP + m] = 0;
     for (int j = 0; j < p.D; j++)
       if (!pm.lin_small[m * p.D + j]) pm.tg_used[p.NP + m] = 1;
   }
-  pl->have_constants = true;
-  return MPT_OK;
+  return choose_kernel(pl, pl->requested_kernel, pl->requested_cluster);
 }
 
 static int ensure_rec(mpt_plan* pl, size_t slots) {
@@ -357,7 +384,9 @@ static int launch(mpt_plan* pl, int n_steps, int start_step, int stride, cudaStr
   p.rec = pl->d_rec;
   p.counters = pl->counting ? pl->d_counters : nullptr;
   CK(cudaEventRecord(pl->ev0, stream));
-  if (pl->kernel == 2)
+  if (pl->kernel == 3)
+    CK(mpt::launch_pipe_kernel(p, pl->cluster, pl->smem_cluster, stream));
+  else if (pl->kernel == 2)
     CK(mpt::launch_cluster_kernel(p, pl->cluster, pl->smem_cluster, stream));
   else
     CK(mpt::launch_team_kernel(p, pl->smem, stream));

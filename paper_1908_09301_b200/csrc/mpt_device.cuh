@@ -289,8 +289,24 @@ __device__ inline void round_to_prec(int32_t* out, int W, int prec_bits, bool& o
   if (cin) ovf = true;
 }
 
+template <int MAXM>
+__device__ __forceinline__ bool warp_normalize_upto(const int64_t* col, int ncols, int drop, int W, int32_t* out,
+                                                   int2* info, int round_prec_bits);
+
 __device__ __forceinline__ bool warp_normalize(const int64_t* col, int ncols, int drop, int W, int32_t* out, int2* info,
                                       int round_prec_bits) {
+  return warp_normalize_upto<kMaxLanesDigits>(col, ncols, drop, W, out, info, round_prec_bits);
+}
+
+// ncols <= 256 (<= 8 digits per lane): fewer instantiations, fewer registers
+__device__ __forceinline__ bool warp_normalize_small(const int64_t* col, int ncols, int drop, int W, int32_t* out,
+                                                     int2* info, int round_prec_bits) {
+  return warp_normalize_upto<8>(col, ncols, drop, W, out, info, round_prec_bits);
+}
+
+template <int MAXM>
+__device__ __forceinline__ bool warp_normalize_upto(const int64_t* col, int ncols, int drop, int W, int32_t* out,
+                                                   int2* info, int round_prec_bits) {
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int m = (ncols + 31) / 32;
@@ -299,12 +315,12 @@ __device__ __forceinline__ bool warp_normalize(const int64_t* col, int ncols, in
     ovf = warp_normalize_t<2>(col, ncols, drop, W, out);
   else if (m <= 4)
     ovf = warp_normalize_t<4>(col, ncols, drop, W, out);
-  else if (m <= 8)
-    ovf = warp_normalize_t<8>(col, ncols, drop, W, out);
-  else if (m <= 16)
-    ovf = warp_normalize_t<16>(col, ncols, drop, W, out);
+  else if (MAXM <= 8 || m <= 8)
+    ovf = warp_normalize_t<(MAXM < 8 ? MAXM : 8)>(col, ncols, drop, W, out);
+  else if (MAXM <= 16 || m <= 16)
+    ovf = warp_normalize_t<(MAXM < 16 ? MAXM : 16)>(col, ncols, drop, W, out);
   else
-    ovf = warp_normalize_t<kMaxLanesDigits>(col, ncols, drop, W, out);
+    ovf = warp_normalize_t<MAXM>(col, ncols, drop, W, out);
   __syncwarp();
   if (round_prec_bits > 0) {
     if (lane == 0) round_to_prec(out, W, round_prec_bits, ovf);

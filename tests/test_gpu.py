@@ -50,7 +50,7 @@ def test_integrate_bit_exact_vs_model(gpu, P, N, steps, stride):
 
 
 @pytest.mark.parametrize("kernel,cluster", [("team", 1), ("cluster", 1), ("cluster", 2), ("cluster", 8),
-                                            ("cluster", 16)])
+                                            ("cluster", 16), ("pipe", 1), ("pipe", 2), ("pipe", 4), ("pipe", 16)])
 @pytest.mark.parametrize("P,N,steps", [(167, 40, 12), (1661, 200, 2)])
 def test_every_kernel_bit_exact_vs_model(gpu, kernel, cluster, P, N, steps):
     ctx, system, fmt, tables = lorenz_tables(P, N)
