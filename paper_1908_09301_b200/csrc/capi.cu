@@ -260,7 +260,7 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
 }
 
 int mpt_plan_configure(mpt_plan* pl, int kernel, int cluster) {
-  if (!pl || kernel < 0 || kernel > 2 || cluster < 1 || cluster > 16) return fail(MPT_EINVAL, "bad configuration");
+  if (!pl || kernel < 0 || kernel > 3 || cluster < 1 || cluster > 16) return fail(MPT_EINVAL, "bad configuration");
   return choose_kernel(pl, kernel, cluster);
 }
 
