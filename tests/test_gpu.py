@@ -59,7 +59,7 @@ def test_every_kernel_bit_exact_vs_model(gpu, kernel, cluster, P, N, steps):
         try:
             plan.configure(kernel, cluster)
         except Exception as exc:  # rows do not fit this cluster size's shared memory
-            assert "shared memory" in str(exc)
+            assert "shared memory" in str(exc) or "does not support" in str(exc)
             pytest.skip(str(exc))
         info = plan.info()
         assert info["kernel"] == kernel
