@@ -277,6 +277,10 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_pipe_kernel(const __grid_c
 
     for (int i = 0; i < p.N; i++) {
       const int par = i & 1;
+      const bool tlog = p.dbg && n == p.start_step + 1 && rank == 0 && i < 200 && lane == 0;
+#define TSTAMP(ev) \
+  if (tlog) p.dbg[(size_t)i * 16 + (ev)] = (long long)clock64();
+      if (warp == 0) TSTAMP(0);
       if (is_chain) {
         // ================= chain ================================================
         const int32_t* cur = CROW(CR_CUR + par * p.D);  // coefficient i, variable 0
@@ -303,6 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_pipe_kernel(const __grid_c
           s_np = np;
         }
         asm volatile("bar.sync 1, %0;" ::"r"(32 * kChainWarps));
+        if (warp == 0) TSTAMP(1);
         // C1: chain products, one warp per product
         const int npr = s_np;
         for (int pr = warp; pr < npr; pr += kChainWarps) {
@@ -334,6 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_pipe_kernel(const __grid_c
                        wcar + (size_t)warp * kPch * (g.NGb + 1), prod + (size_t)pr * g.NCX, false, mc);
         }
         asm volatile("bar.sync 1, %0;" ::"r"(32 * kChainWarps));
+        if (warp == 0) TSTAMP(2);
         // C2 + C3: warp m owns equation m
         for (int m = warp; m < p.D; m += kChainWarps) {
           int64_t* uc = ucol + (size_t)warp * g.NCX;
@@ -363,15 +369,19 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_pipe_kernel(const __grid_c
             uc[c] = s;
           }
           __syncwarp();
+          if (warp == 2) TSTAMP(3);
           if (warp_normalize_small(uc, g.ncolb, 2, p.W, CROW(CR_U + m), &cinfo[CR_U + m], 0) && lane == 0) flag[0] = 1;
+          if (warp == 2) TSTAMP(4);
           // C3: scale by tau/(i+1)
           const int32_t* ct = CROW(CR_CT + par);
           const int2 ctinf = row_info_warp(ct, p.W);
           warp_product(CROW(CR_U + m), cinfo[CR_U + m], ct, ctinf, g.Tc, g.gfc, g.NGc, g.ncolc, g.NCX,
                        wsc + (size_t)warp * kPch * g.NCX, wcar + (size_t)warp * kPch * (g.NGb + 1), uc, false, mc);
+          if (warp == 2) TSTAMP(5);
           int32_t* nxt = CROW(CR_CUR + (par ^ 1) * p.D + m);
           if (warp_normalize_small(uc, g.ncolc, 2, p.W, nxt, &cinfo[CR_CUR + (par ^ 1) * p.D + m], 0) && lane == 0)
             flag[0] = 1;
+          if (warp == 2) TSTAMP(6);
           // publish: rows for the bulk warps (after the barrier), state sums
           const bool keep = has_row(m, i + 1);
           int32_t* dst = keep ? ROW(m, i + 1) : nullptr;
@@ -440,7 +450,9 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_pipe_kernel(const __grid_c
             }
           }
         }
+        if (warp == kChainWarps) TSTAMP(8);
         asm volatile("bar.sync 2, %0;" ::"r"(32 * kBulkWarps));
+        if (warp == kChainWarps) TSTAMP(9);
         // reduce the slots and push the totals into every CTA's receive slot [rank]
         const size_t rbase = (size_t)(par ^ 1) * recv_par;
         for (int w = bt; w < p.NP * g.ncolb; w += 32 * kBulkWarps) {
@@ -452,7 +464,11 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_pipe_kernel(const __grid_c
         }
       }
       // one cluster barrier per order: P(i+1) pushed, coefficient i+1 published
+      if (warp == 2) TSTAMP(7);
+      if (warp == kChainWarps) TSTAMP(10);
       cluster.sync();
+      if (warp == 0) TSTAMP(11);
+#undef TSTAMP
     }
     // ---- end of step: state = RN_P(sum of rows) --------------------------------
     if (is_chain) {
