@@ -70,7 +70,7 @@ struct Layout {
 // k = rank (mod G).
 __host__ __device__ inline Layout make_layout(const Params& p, int G) {
   Layout L;
-  L.rs = (p.W + 3) / 4 * 4 + kPad;
+  L.rs = (p.W + 3) / 4 * 4 + kPad + 1;  // odd: k-slots hit different banks
   int s = 0;
   for (int v = 0; v < p.D; v++) {
     int is_left = 0;

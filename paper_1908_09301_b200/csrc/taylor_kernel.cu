@@ -27,7 +27,8 @@
 namespace mpt {
 
 __host__ __device__ inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
-__host__ __device__ inline int row_words(int RS) { return RS + 2 * kPad; }
+// odd row stride: consecutive k-slots fall into different shared-memory banks
+__host__ __device__ inline int row_words(int RS) { return RS + 2 * kPad + 1; }
 
 struct Geo {
   int Tb, gfb, NGb;  // base products: first column, first group, #groups
@@ -220,7 +221,12 @@ __global__ void __launch_bounds__(256, 1) taylor_team_kernel(const __grid_consta
               const int kk = r / nrows, v = r - kk * nrows;
               const int k = k0 + kk;
               const int32_t* src = v < p.nlv ? GROW(p.lvar[v], i - k) : GROW(p.rvar[v - p.nlv], k);
-              reinterpret_cast<int4*>(ROW(stage, r))[w] = __ldcg(reinterpret_cast<const int4*>(src) + w);
+              const int4 v4 = __ldcg(reinterpret_cast<const int4*>(src) + w);
+              int32_t* dst = ROW(stage, r) + 4 * w;
+              dst[0] = v4.x;
+              dst[1] = v4.y;
+              dst[2] = v4.z;
+              dst[3] = v4.w;
             }
             for (int r = tid; r < kcn * nrows; r += nt) {
               const int kk = r / nrows, v = r - kk * nrows;

@@ -71,7 +71,7 @@ struct Layout {
 // crow rows: cst D | lin D*D | q NT | ctab x2 | U D | CUR x2 (D each) | ZERO D
 __host__ __device__ inline Layout make_layout(const Params& p, int G) {
   Layout L;
-  L.rs = (p.W + 3) / 4 * 4 + kPad;
+  L.rs = (p.W + 3) / 4 * 4 + kPad + 1;  // odd: k-slots hit different banks
   int s = 0;
   for (int v = 0; v < p.D; v++) {
     int is_left = 0;
