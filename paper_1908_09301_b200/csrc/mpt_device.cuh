@@ -65,9 +65,7 @@ __device__ __forceinline__ unsigned useful_macs(int2 ia, int2 ib, int c0, int tc
   return n;
 }
 
-// Not inlined on purpose: the unrolled 8x8 body is large and is called from
-// several phases; one copy keeps the kernels inside the instruction cache.
-static __device__ __noinline__ void mac_group(Acc& acc, int& cnt, const int32_t* __restrict__ A, int2 ia,
+__device__ __forceinline__ void mac_group(Acc& acc, int& cnt, const int32_t* __restrict__ A, int2 ia,
                                        const int32_t* __restrict__ B, int2 ib, int c0, int tcut,
                                        MacCount* mc = nullptr) {
   // nonzero digits: A in [ia.x, ia.y], B in [ib.x, ib.y]
@@ -292,7 +290,7 @@ __device__ inline void round_to_prec(int32_t* out, int W, int prec_bits, bool& o
 }
 
 template <int MAXM>
-static __device__ __noinline__ bool warp_normalize_upto(const int64_t* col, int ncols, int drop, int W, int32_t* out,
+__device__ __forceinline__ bool warp_normalize_upto(const int64_t* col, int ncols, int drop, int W, int32_t* out,
                                                 int2* info, int round_prec_bits);
 
 __device__ __forceinline__ bool warp_normalize(const int64_t* col, int ncols, int drop, int W, int32_t* out, int2* info,
@@ -307,7 +305,7 @@ __device__ __forceinline__ bool warp_normalize_small(const int64_t* col, int nco
 }
 
 template <int MAXM>
-static __device__ __noinline__ bool warp_normalize_upto(const int64_t* col, int ncols, int drop, int W, int32_t* out,
+__device__ __forceinline__ bool warp_normalize_upto(const int64_t* col, int ncols, int drop, int W, int32_t* out,
                                                 int2* info, int round_prec_bits) {
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;

@@ -145,7 +145,7 @@ __device__ __forceinline__ int64_t unit_col(const uint32_t* part, const int64_t*
 // One warp computes the truncated product A (x) B into columns out[0..ncol)
 // (relative to T): lanes = (column group, p-chunk), partials through a
 // warp-private scratch, then one column sum per lane. `acc_into` adds.
-__device__ __noinline__ void warp_product(const int32_t* A, int2 ia, const int32_t* B, int2 ib, int T, int gf,
+__device__ __forceinline__ void warp_product(const int32_t* A, int2 ia, const int32_t* B, int2 ib, int T, int gf,
                                              int ng, int ncol, int ncx, uint32_t* wsc, int64_t* wcar, int64_t* out,
                                              bool acc_into, MacCount* mc) {
   const int lane = threadIdx.x & 31;
