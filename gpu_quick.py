@@ -15,6 +15,9 @@ def perf(K, N, steps, configs):
             plan.upload(st); plan.run_device(2); plan.last_kernel_ms()
             plan.count_macs(True); plan.run_device(steps); ms=plan.last_kernel_ms(); u,x=plan.read_macs()
             print(f'K={K} N={N} {plan.info()} : {ms/steps:.3f} ms/step = {1000*steps/ms:.1f} steps/s; useful MAC/step {u/steps:.3e} executed {x/steps:.3e}', flush=True)
-perf(50,40,100,[('cluster',1),('pipe',1),('pipe',2),('pipe',4),('pipe',8),('pipe',16)])
-perf(500,200,20,[('cluster',16),('pipe',2),('pipe',4),('pipe',8),('pipe',16)])
-perf(800,480,2,[('team',1),('pipe',8),('pipe',16)])
+perf(50,40,100,[('pipe',1)])
+perf(500,200,20,[('cluster',16),('pipe',16)])
+perf(500,200,20,[('grid',1)])
+perf(800,480,2,[('team',1),('grid',1)])
+perf(2200,1000,1,[('grid',1)])
+perf(4200,3500,1,[('grid',1)])

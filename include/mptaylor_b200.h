@@ -65,9 +65,10 @@ int mpt_plan_destroy(mpt_plan *plan);
  * kernel when the coefficient rows fit, with an 8-CTA cluster per trajectory
  * for single-trajectory plans; otherwise the team kernel with rows in HBM).
  * kernel: 0 auto, 1 team (rows in HBM/L2), 2 cluster (rows in smem),
- *         3 pipelined cluster kernel (warp-specialised lookahead, single trajectories);
+ *         3 pipelined cluster kernel (warp-specialised lookahead, single trajectories),
+ *         4 grid kernel (one trajectory on every SM, rows in L2; large precision);
  * cluster: CTAs per trajectory (1..16) for the cluster kernel.
- * Environment overrides at plan creation: MPT_KERNEL=team|cluster|pipe, MPT_CLUSTER=G. */
+ * Environment overrides at plan creation: MPT_KERNEL=team|cluster|pipe|grid, MPT_CLUSTER=G. */
 int mpt_plan_configure(mpt_plan *plan, int kernel, int cluster);
 int mpt_plan_kernel(const mpt_plan *plan, int *kernel, int *cluster);
 

@@ -22,6 +22,11 @@ size_t pipe_smem_bytes(const Params& p, int G);
 bool pipe_supported(const Params& p);
 cudaError_t launch_pipe_kernel(const Params& p, int G, size_t smem, cudaStream_t stream);
 int pipe_max_cluster(const Params& p, size_t smem, int want);
+bool grid_supported(const Params& p);
+size_t grid_smem_bytes(const Params& p, int kc);
+size_t grid_scratch_bytes(const Params& p);
+cudaError_t launch_grid_kernel(const Params& p, int nblocks, int kc, size_t smem, cudaStream_t stream);
+int grid_max_blocks(const Params& p, size_t smem);
 }  // namespace mpt
 
 static thread_local std::string g_err;
@@ -53,12 +58,37 @@ struct mpt_plan {
   bool have_constants = false;
   unsigned long long* d_counters = nullptr;
   bool counting = false;
-  int kernel = 0;    // 1 = team kernel (rows in HBM/L2), 2 = cluster kernel (rows in smem), 3 = pipeline
+  int kernel = 0;    // 1 team (rows in HBM/L2), 2 cluster (rows in smem), 3 pipeline, 4 grid (all SMs)
   int cluster = 1;   // CTAs per trajectory for the cluster kernel
   size_t smem_cluster = 0;
   int optin = 0;
   int requested_kernel = 0, requested_cluster = 1;
+  int grid_blocks = 0, grid_kc = 0;
+  size_t smem_grid = 0;
+  void* d_gscratch = nullptr;
 };
+
+static int setup_grid(mpt_plan* pl) {
+  mpt::Params& p = pl->p;
+  int kc = 64;
+  size_t s = 0;
+  for (; kc >= 1; kc = kc > 8 ? kc - 8 : kc - 1) {
+    s = mpt::grid_smem_bytes(p, kc);
+    if (s <= (size_t)pl->optin) break;
+  }
+  if (kc < 1) return fail(MPT_EUNSUP, "grid kernel: shared memory budget exceeded");
+  int nb = mpt::grid_max_blocks(p, s);
+  if (nb < 1) return fail(MPT_EUNSUP, "grid kernel: no co-resident blocks");
+  if (!pl->d_gscratch) {
+    CK(cudaMalloc(&pl->d_gscratch, mpt::grid_scratch_bytes(p)));
+    CK(cudaMemset(pl->d_gscratch, 0, mpt::grid_scratch_bytes(p)));
+  }
+  p.gscratch = pl->d_gscratch;
+  pl->grid_blocks = nb;
+  pl->grid_kc = kc;
+  pl->smem_grid = s;
+  return MPT_OK;
+}
 
 // choose the kernel: the smem-resident cluster kernel when the rows fit,
 // one cluster of `want` CTAs per trajectory (clamped to what co-schedules)
@@ -69,6 +99,18 @@ static int choose_kernel(mpt_plan* pl, int kernel, int want) {
   if (kernel == 1) {
     pl->kernel = 1;
     pl->cluster = 1;
+    return MPT_OK;
+  }
+  if (kernel == 4) {
+    if (!pl->have_constants) {
+      pl->kernel = 0;
+      return MPT_OK;
+    }
+    if (!mpt::grid_supported(p)) return fail(MPT_EUNSUP, "grid kernel: one trajectory, integer bilinear coefficients");
+    int rc = setup_grid(pl);
+    if (rc) return rc;
+    pl->kernel = 4;
+    pl->cluster = pl->grid_blocks;
     return MPT_OK;
   }
   const int tries[] = {16, 8, 4, 2, 1};
@@ -103,6 +145,11 @@ static int choose_kernel(mpt_plan* pl, int kernel, int want) {
     return MPT_OK;
   }
   if (kernel == 2) return fail(MPT_EUNSUP, "coefficient rows do not fit shared memory for the cluster kernel");
+  if (kernel == 0 && pl->have_constants && mpt::grid_supported(p) && setup_grid(pl) == MPT_OK) {
+    pl->kernel = 4;
+    pl->cluster = pl->grid_blocks;
+    return MPT_OK;
+  }
   pl->kernel = 1;
   pl->cluster = 1;
   return MPT_OK;
@@ -247,7 +294,12 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
   {
     const char* ek = getenv("MPT_KERNEL");
     const char* ec = getenv("MPT_CLUSTER");
-    int kernel = ek ? (strcmp(ek, "team") == 0 ? 1 : strcmp(ek, "cluster") == 0 ? 2 : strcmp(ek, "pipe") == 0 ? 3 : 0) : 0;
+    int kernel = ek ? (strcmp(ek, "team") == 0      ? 1
+                       : strcmp(ek, "cluster") == 0 ? 2
+                       : strcmp(ek, "pipe") == 0    ? 3
+                       : strcmp(ek, "grid") == 0    ? 4
+                                                    : 0)
+                    : 0;
     int want = ec ? atoi(ec) : (n_traj == 1 ? 16 : 1);
     int rc = choose_kernel(pl, kernel, want < 1 ? 1 : want);
     if (rc) {
@@ -260,7 +312,7 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
 }
 
 int mpt_plan_configure(mpt_plan* pl, int kernel, int cluster) {
-  if (!pl || kernel < 0 || kernel > 3 || cluster < 1 || cluster > 16) return fail(MPT_EINVAL, "bad configuration");
+  if (!pl || kernel < 0 || kernel > 4 || cluster < 1 || cluster > 16) return fail(MPT_EINVAL, "bad configuration");
   return choose_kernel(pl, kernel, cluster);
 }
 
@@ -283,6 +335,7 @@ int mpt_plan_destroy(mpt_plan* pl) {
   cudaFree(pl->d_rec);
   cudaFree(pl->d_status);
   cudaFree(pl->d_counters);
+  cudaFree(pl->d_gscratch);
   if (pl->ev0) cudaEventDestroy(pl->ev0);
   if (pl->ev1) cudaEventDestroy(pl->ev1);
   delete pl;
@@ -293,7 +346,11 @@ int mpt_plan_width(const mpt_plan* pl) { return pl ? pl->W : MPT_EINVAL; }
 
 int mpt_plan_info(const mpt_plan* pl, int* smem_bytes, int* k_chunk, int* threads) {
   if (!pl) return MPT_EINVAL;
-  if (smem_bytes) *smem_bytes = (int)(pl->kernel >= 2 ? pl->smem_cluster : pl->smem);
+  if (smem_bytes) *smem_bytes = (int)(pl->kernel == 4 ? pl->smem_grid : pl->kernel >= 2 ? pl->smem_cluster : pl->smem);
+  if (k_chunk && pl->kernel == 4) {
+    *k_chunk = pl->grid_kc;
+    k_chunk = nullptr;
+  }
   if (k_chunk) *k_chunk = pl->p.kc;
   if (threads) *threads = pl->p.nthreads;
   return MPT_OK;
@@ -384,7 +441,12 @@ static int launch(mpt_plan* pl, int n_steps, int start_step, int stride, cudaStr
   p.rec = pl->d_rec;
   p.counters = pl->counting ? pl->d_counters : nullptr;
   CK(cudaEventRecord(pl->ev0, stream));
-  if (pl->kernel == 3)
+  if (pl->kernel == 4) {
+    CK(cudaMemsetAsync(pl->d_gscratch, 0, mpt::grid_scratch_bytes(p), stream));
+    CK(cudaMemsetAsync(pl->d_status, 0, sizeof(int32_t) * p.n_traj, stream));
+    p.gscratch = pl->d_gscratch;
+    CK(mpt::launch_grid_kernel(p, pl->grid_blocks, pl->grid_kc, pl->smem_grid, stream));
+  } else if (pl->kernel == 3)
     CK(mpt::launch_pipe_kernel(p, pl->cluster, pl->smem_cluster, stream));
   else if (pl->kernel == 2)
     CK(mpt::launch_cluster_kernel(p, pl->cluster, pl->smem_cluster, stream));

@@ -62,6 +62,7 @@ struct Params {
   unsigned long long* counters;  // optional: [0] useful limb-MACs, [1] executed limb-MACs
   int write_coef;                // cluster kernel: also store every coefficient row to `coef`
   long long* dbg;                // debug dump (nullptr in production)
+  void* gscratch;                // grid kernel: global accumulators + barrier words
 };
 
 }  // namespace mpt

@@ -50,7 +50,8 @@ def test_integrate_bit_exact_vs_model(gpu, P, N, steps, stride):
 
 
 @pytest.mark.parametrize("kernel,cluster", [("team", 1), ("cluster", 1), ("cluster", 2), ("cluster", 8),
-                                            ("cluster", 16), ("pipe", 1), ("pipe", 2), ("pipe", 4), ("pipe", 16)])
+                                            ("cluster", 16), ("pipe", 1), ("pipe", 2), ("pipe", 4), ("pipe", 16),
+                                            ("grid", 1)])
 @pytest.mark.parametrize("P,N,steps", [(167, 40, 12), (1661, 200, 2)])
 def test_every_kernel_bit_exact_vs_model(gpu, kernel, cluster, P, N, steps):
     ctx, system, fmt, tables = lorenz_tables(P, N)
@@ -66,6 +67,21 @@ def test_every_kernel_bit_exact_vs_model(gpu, kernel, cluster, P, N, steps):
         s_gpu, r_gpu, status = plan.integrate(st, steps, 0, 1)
     s_cpu, r_cpu = FX.integrate(tables, fmt.frac_digits, N, P, st, steps, 0, 1)
     assert np.array_equal(r_gpu[:, 0], r_cpu), info
+
+
+@pytest.mark.parametrize("K,N,steps", [(2200, 40, 2), (4200, 12, 1)])
+def test_grid_kernel_large_precision_bit_exact(gpu, K, N, steps):
+    P = M.bits_for_digits(K)
+    ctx, system, fmt, tables = lorenz_tables(P, N)
+    st = fmt.to_digits([M.mp_from_decimal(t, ctx) for t in CANON_INIT])
+    with DevicePlan(tables, fmt, N, 1) as plan:
+        plan.configure("grid", 1)
+        assert plan.info()["kernel"] == "grid"
+        _, r_gpu, status = plan.integrate(st, steps, 0, 1)
+        jet = plan.compute_jet(st)[0]
+    _, r_cpu = FX.integrate(tables, fmt.frac_digits, N, P, st, steps, 0, 1)
+    assert np.array_equal(r_gpu[:, 0], r_cpu)
+    assert np.array_equal(jet, FX.compute_jet(tables, fmt.frac_digits, N, st))
 
 
 def test_jet_bit_exact_vs_model_large_order(gpu):
