@@ -29,7 +29,7 @@
 namespace mpt {
 namespace grid {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;
 constexpr int kPC = 4;
 
 struct Geo {
@@ -210,6 +210,10 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
     __syncthreads();
     for (int i = 0; i < p.N; i++) {
       const long long gord = (long long)(n - p.start_step - 1) * p.N + i;  // launch-wide order counter
+      const bool tlog = p.dbg && n == p.start_step + 1 && b == 0 && tid == 0 && i < 255;
+#define TSTAMP(ev) \
+  if (tlog) p.dbg[(size_t)(i % 256) * 16 + (ev)] = (long long)clock64();
+      TSTAMP(0);
       const int buf = (int)(gord % 3);
       unsigned long long* ua = uacc + (size_t)buf * p.D * g.NCX;
       unsigned long long* ca = cacc + (size_t)buf * p.D * g.NCX;
@@ -279,6 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
           }
         }
       }
+      TSTAMP(1);
       // non-integer linear products: item it -> CTA it % nb
       const int nu_a = ns * p.NP;
       for (int e = tid; e < nlin * g.NGb; e += kThreads) {
@@ -313,7 +318,9 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
             s += unit_col(part, pcar, nu_a + m * p.D + j, 1, 1, g.NCX, L.ngmax, c, g.Tb, g.gfb, g.NGb);
         if (s != 0) atomicAdd(&ua[(size_t)m * g.NCX + c], (unsigned long long)s);
       }
+      TSTAMP(2);
       grid_barrier(bar, bar + 1, nb);
+      TSTAMP(3);
       // ================= phase B: numerators (redundant in every CTA)
       if (b == 0) {  // recycle the buffers of the next order (last read three orders ago)
         unsigned long long* nu2 = uacc + (size_t)((gord + 1) % 3) * p.D * g.NCX;
@@ -338,6 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
         ucol[(size_t)m * g.NCX + c] = s;
       }
       __syncthreads();
+      TSTAMP(4);
       for (int m = warp; m < p.D; m += nwarps)
         if (warp_normalize(ucol + (size_t)m * g.NCX, g.ncolb, 2, p.W, CROW(CR_U + m), &cinfo[CR_U + m], 0) &&
             lane == 0)
@@ -347,6 +355,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
         if (lane == 0) cinfo[CR_CT] = inf;
       }
       __syncthreads();
+      TSTAMP(5);
       // ================= phase C: this CTA's share of U_m (x) tau/(i+1)
       {
         const int nitems = p.D * g.NGc * kPC;
@@ -385,7 +394,9 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
           if (s != 0) atomicAdd(&ca[(size_t)m * g.NCX + c], (unsigned long long)s);
         }
       }
+      TSTAMP(6);
       grid_barrier(bar, bar + 1, nb);
+      TSTAMP(7);
       // ================= phase D: coefficient i+1 (redundant), CTA 0 publishes
       for (int w = tid; w < p.D * g.ncolc; w += kThreads) {
         const int m = w / g.ncolc, c = w - m * g.ncolc;
@@ -397,17 +408,17 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
             lane == 0)
           flag[0] = 1;
       __syncthreads();
+      TSTAMP(8);
       for (int m = warp; m < p.D; m += nwarps) {
         for (int d = lane; d < p.W; d += 32) ssum[(size_t)m * (p.W + 3) + d] += CROW(CR_CUR + m)[d];
         if (b == 0) {
           for (int d = lane; d < p.RS; d += 32) GROW(m, i + 1)[d] = d < p.W ? CROW(CR_CUR + m)[d] : 0;
           if (lane == 0) GINF(m, i + 1) = cinfo[CR_CUR + m];
-          if (p.write_coef) {
-            // the coefficient table IS p.coef here: nothing extra to store
-          }
         }
       }
       __syncthreads();
+      TSTAMP(9);
+#undef TSTAMP
     }
     // state = RN_P(sum of the rows)
     for (int m = warp; m < p.D; m += nwarps)
