@@ -99,77 +99,114 @@ __device__ __forceinline__ void mac_group(Acc& acc, int& cnt, const int32_t* __r
   }
 }
 
+// mac_group restricted to chunk `pc` of `pch` near-equal runs of whole kR
+// blocks of the p range: lets several threads share one (row pair, group).
+__device__ __forceinline__ void mac_group_chunk(Acc& acc, int& cnt, const int32_t* __restrict__ A, int2 ia,
+                                                const int32_t* __restrict__ B, int2 ib, int c0, int tcut, int pc,
+                                                int pch, MacCount* mc) {
+  if (pch > 1) {
+    const int plo = max(ia.x, c0 - ib.y), phi = min(ia.y, c0 + kR - 1 - ib.x);
+    if (plo > phi) return;
+    const int b0 = plo / kR, nb = phi / kR - b0 + 1;
+    const int per = (nb + pch - 1) / pch;
+    const int blo = b0 + pc * per, bhi = min(b0 + nb, blo + per) - 1;
+    if (blo > bhi) return;
+    ia.x = max(ia.x, blo * kR);
+    ia.y = min(ia.y, bhi * kR + kR - 1);
+  }
+  mac_group(acc, cnt, A, ia, B, ib, c0, tcut, mc);
+}
+
 // ---------------------------------------------------------------------------
 // Warp-cooperative normalisation of a column vector (relative columns
 // 0..ncols-1, value V = sum col[c] B^c, |col[c]| < 2^62) into canonical signed
 // digits of floor((V + [drop] B^drop / 2) / B^drop), drop in {0, 2}.
-// Lane l holds columns [l*m, l*m+m). Carries are resolved without
-// data-dependent loops: one local pass, two shuffle passes (carries shrink to
-// {-1, 0, +1}), then a ballot carry-lookahead per sign:
-//   carry-in mask C = (((A & P) + P) ^ P) | A,  A = lanes receiving a carry,
-//   P = lanes whose block would pass it on (all digits B-1, or all 0 for borrows).
+// Lane l holds columns [l*m, l*m+m). No data-dependent loops and no long
+// per-lane dependency chains:
+//   * three rounds of "split every column into digit + carry, add the carry to
+//     the next column" (all columns in parallel) leave digits in [-1, B];
+//   * one carry-lookahead per sign resolves the remaining +1 / -1 ripples:
+//     inside a lane with m-bit generate/propagate masks,
+//         C = (((A & P) + P) ^ P) | A,   A = (G << 1) | carry_in,
+//     and across lanes with the same identity on __ballot_sync masks.
 template <int MM>
 struct Blk {
   int64_t v[MM];
 };
 
-// add `cin` to the block (digit 0 upward); digits back to [0, B); returns carry out
+// three parallel carry rounds; returns what leaves lane 31 (warp-uniform)
 template <int MM>
-__device__ __forceinline__ int64_t blk_add(Blk<MM>& b, int m, int64_t cin) {
+__device__ __forceinline__ int64_t blk_rounds(Blk<MM>& b, int m) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  int64_t top = 0;
+#pragma unroll
+  for (int rnd = 0; rnd < 3; rnd++) {
+    int64_t c[MM];
+    int64_t cout = 0;
+#pragma unroll
+    for (int j = 0; j < MM; j++) {
+      c[j] = 0;
+      if (j < m) {
+        const int64_t v = b.v[j];
+        const int64_t dg = v & kMask;
+        c[j] = (v - dg) >> kRadixBits;
+        b.v[j] = dg;
+        if (j == m - 1) cout = c[j];
+      }
+    }
+    int64_t cin = __shfl_up_sync(full, cout, 1);
+    top += __shfl_sync(full, cout, 31);
+    if (lane == 0) cin = 0;
+#pragma unroll
+    for (int j = MM - 1; j >= 1; j--)
+      if (j < m) b.v[j] += c[j - 1];
+    b.v[0] += cin;
+  }
+  return top;
+}
+
+// resolve pending +1 (sgn > 0: digits >= B generate, == B-1 propagate) or
+// -1 (digits < 0 generate, == 0 propagate) carries; returns the signed carry
+// that leaves lane 31
+template <int MM>
+__device__ __forceinline__ int64_t blk_lookahead(Blk<MM>& b, int m, int sgn) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  uint32_t G = 0, P = 0;
 #pragma unroll
   for (int j = 0; j < MM; j++) {
     if (j < m) {
-      const int64_t t = b.v[j] + cin;
-      const int64_t dgt = t & kMask;
-      cin = (t - dgt) >> kRadixBits;
-      b.v[j] = dgt;
+      const int64_t v = b.v[j];
+      const bool g = sgn > 0 ? (v >= kRadix) : (v < 0);
+      const bool pr = sgn > 0 ? (v == kMask) : (v == 0);
+      G |= (uint32_t)g << j;
+      P |= (uint32_t)pr << j;
     }
   }
-  return cin;
-}
-
-template <int MM>
-__device__ __forceinline__ bool blk_all(const Blk<MM>& b, int m, int64_t val) {
-  bool all = true;
+  const uint32_t allp = (m >= 32) ? 0xffffffffu : ((1u << m) - 1u);
+  auto local = [&](uint32_t cin) -> uint64_t {
+    const uint64_t A = ((uint64_t)G << 1) | cin;
+    const uint64_t S = (A & P) + P;
+    return (S ^ P) | A;  // bit j: carry into digit j; bit m: carry out of the lane
+  };
+  const uint64_t C0 = local(0);
+  const uint32_t Gl = __ballot_sync(full, (C0 >> m) & 1);
+  const uint32_t Pl = __ballot_sync(full, P == allp);
+  const uint64_t A = ((uint64_t)Gl << 1) & 0xffffffffull;
+  const uint64_t S = (A & Pl) + Pl;
+  const uint32_t Cin = ((uint32_t)S ^ Pl) | (uint32_t)A;
+  const int64_t out31 = (int64_t)(((S >> 32) & 1) | ((Gl >> 31) & 1));
+  const uint64_t C = local((Cin >> lane) & 1);
 #pragma unroll
-  for (int j = 0; j < MM; j++)
-    if (j < m) all &= (b.v[j] == val);
-  return all;
-}
-
-// resolve pending carries e (from this lane into the next) in {-1, 0, 1};
-// `top` collects what leaves lane 31
-template <int MM>
-__device__ __forceinline__ void blk_resolve(Blk<MM>& b, int m, int e, int64_t& top) {
-  const unsigned full = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  const int ein = __shfl_up_sync(full, e, 1);
-  const int e31 = __shfl_sync(full, e, 31);
-  top += e31;
-#pragma unroll
-  for (int sgn = 1; sgn >= -1; sgn -= 2) {
-    const unsigned A = __ballot_sync(full, lane > 0 && ein == sgn);
-    const unsigned P = __ballot_sync(full, blk_all(b, m, sgn > 0 ? kMask : 0));
-    const unsigned long long S = (unsigned long long)(A & P) + P;
-    const unsigned C = ((unsigned)S ^ P) | A;
-    top += sgn * (int64_t)(S >> 32);
-    if ((C >> lane) & 1u) blk_add(b, m, sgn);
+  for (int j = 0; j < MM; j++) {
+    if (j < m) {
+      const int64_t cj = (C >> j) & 1;
+      const int64_t oj = ((G >> j) & 1) | (((P >> j) & 1) & cj);
+      b.v[j] += sgn > 0 ? (cj - kRadix * oj) : (kRadix * oj - cj);
+    }
   }
-}
-
-template <int MM>
-__device__ __forceinline__ void blk_carry(Blk<MM>& b, int m, int64_t& top) {
-  const unsigned full = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  int64_t c = blk_add(b, m, 0);
-#pragma unroll
-  for (int pass = 0; pass < 2; pass++) {
-    int64_t cin = __shfl_up_sync(full, c, 1);
-    top += __shfl_sync(full, c, 31);
-    if (lane == 0) cin = 0;
-    c = blk_add(b, m, cin);
-  }
-  blk_resolve(b, m, (int)c, top);
+  return sgn * out31;
 }
 
 template <int MM>
@@ -184,56 +221,21 @@ __device__ __forceinline__ bool warp_normalize_t(const int64_t* col, int ncols, 
     b.v[j] = (j < m && c < ncols) ? col[c] : 0;
     if (drop && c == drop - 1) b.v[j] += kRadix / 2;  // rounding: + B^drop / 2
   }
-  int64_t top = 0;
-  blk_carry(b, m, top);  // digits in [0, B), signed carry in `top`
-  if (drop) {
+  int64_t top = blk_rounds(b, m);  // digits in [-1, B]
+  top += blk_lookahead(b, m, 1);
+  top += blk_lookahead(b, m, -1);  // canonical digits in [0, B), signed carry in `top`
 #pragma unroll
-    for (int j = 0; j < MM; j++)
-      if (lane * m + j < drop) b.v[j] = 0;  // floor: discard the low digits
-  }
-  if (false) {
-    // + B^drop / 2 == + B/2 at column drop-1, then floor: discard columns < drop
-    int e = 0;
-    if (lane * m <= drop - 1 && drop - 1 < lane * m + m) {
-      int64_t cin = 0;
-#pragma unroll
-      for (int j = 0; j < MM; j++) {
-        if (j < m) {
-          const int64_t t = b.v[j] + cin + ((lane * m + j == drop - 1) ? (kRadix / 2) : 0);
-          const int64_t dgt = t & kMask;
-          cin = (t - dgt) >> kRadixBits;
-          b.v[j] = dgt;
-        }
-      }
-      e = (int)cin;
-    }
-    blk_resolve(b, m, e, top);
-#pragma unroll
-    for (int j = 0; j < MM; j++)
-      if (lane * m + j < drop) b.v[j] = 0;
-  }
+  for (int j = 0; j < MM; j++)
+    if (lane * m + j < drop) b.v[j] = 0;  // floor: discard the dropped digits
   const bool neg = top < 0;
   if (neg) {
     // |R| = -R: complement the kept digits and add one at column `drop`
-    int e = 0;
 #pragma unroll
-    for (int j = 0; j < MM; j++)
-      if (j < m && lane * m + j >= drop) b.v[j] = kMask - b.v[j];
-    top = -top - 1;
-    if (lane * m <= drop && drop < lane * m + m) {
-      int64_t cin = 0;
-#pragma unroll
-      for (int j = 0; j < MM; j++) {
-        if (j < m) {
-          const int64_t t = b.v[j] + cin + ((lane * m + j == drop) ? 1 : 0);
-          const int64_t dgt = t & kMask;
-          cin = (t - dgt) >> kRadixBits;
-          b.v[j] = dgt;
-        }
-      }
-      e = (int)cin;
+    for (int j = 0; j < MM; j++) {
+      const int c = lane * m + j;
+      if (j < m && c >= drop) b.v[j] = kMask - b.v[j] + (c == drop ? 1 : 0);
     }
-    blk_resolve(b, m, e, top);
+    top = -top - 1 + blk_lookahead(b, m, 1);
   }
   bool ovf = top != 0;
 #pragma unroll

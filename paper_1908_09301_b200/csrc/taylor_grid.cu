@@ -228,6 +228,8 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
         }
         const int c0 = kR * (g.gfb + grp);
         const int nk = b <= i ? (i - b) / nb + 1 : 0;  // this CTA's k values
+        // few k values: split every product's p range over several slots
+        const int pch = nk > 0 ? max(1, min(16, ns / min(nk, kc))) : 1;
         for (int kk0 = 0; kk0 < nk; kk0 += kc) {
           const int kcn = min(kc, nk - kk0);
           // stage: the newest row (index i) comes from shared memory, older rows from L2
@@ -260,12 +262,13 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
           }
           __syncthreads();
           if (slot < ns) {
-            for (int kk = slot; kk < kcn; kk += ns) {
+            for (int wu = slot; wu < kcn * pch; wu += ns) {
+              const int kk = wu / pch, pc = wu - kk * pch;
 #pragma unroll
               for (int q = 0; q < NPT; q++) {
                 if (q < p.NP) {
                   const int ra = kk * L.nrows + p.pl[q], rb = kk * L.nrows + p.nlv + p.pr[q];
-                  mac_group(acc[q], cnt[q], SROW(ra), stinfo[ra], SROW(rb), stinfo[rb], c0, g.Tb, mc);
+                  mac_group_chunk(acc[q], cnt[q], SROW(ra), stinfo[ra], SROW(rb), stinfo[rb], c0, g.Tb, pc, pch, mc);
                 }
               }
             }
@@ -304,7 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
       __syncthreads();
       // CTA column sums -> numerators U_m (integer q applied) -> RED.ADD.64
       const int nkall = b <= i ? (i - b) / nb + 1 : 0;
-      const int nsa = min(ns, nkall);
+      const int nsa = nkall > 0 ? ns : 0;  // every slot may hold a p-chunk
       for (int w = tid; w < p.D * g.ncolb; w += kThreads) {
         const int m = w / g.ncolb, c = w - m * g.ncolb;
         int64_t s = 0;

@@ -77,7 +77,7 @@ __global__ void k(int W, long long* out) {
 int main() {
   long long* d;
   cudaMalloc(&d, 16);
-  for (int W : {7, 62, 98, 200}) {
+  for (int W : {7, 62, 98, 200, 264, 501}) {
     k<<<1, 32>>>(W, d);
     long long h[2];
     cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
