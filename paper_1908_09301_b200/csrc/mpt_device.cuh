@@ -254,6 +254,159 @@ __device__ __forceinline__ bool warp_normalize_t(const int64_t* col, int ncols, 
   return __any_sync(full, ovf);
 }
 
+// ---------------------------------------------------------------------------
+// Group normalisation: NW warps (named barrier `bar_id`, 32*NW threads) share
+// one column vector; warp w of the group owns columns [w*32*m, (w+1)*32*m).
+// Same algorithm as warp_normalize_t (three parallel carry rounds, then a
+// carry-lookahead per sign), with the warp-to-warp carries exchanged through
+// the shared scratch `xs` (>= 4*NW + 8 int64). Returns the overflow flag.
+__device__ __forceinline__ void group_sync(int bar_id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads));
+}
+
+template <int MM>
+__device__ __forceinline__ int64_t grp_lookahead(Blk<MM>& b, int m, int sgn, int gw, int NW, int bar_id,
+                                                 int64_t* xs) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  uint32_t G = 0, P = 0;
+#pragma unroll
+  for (int j = 0; j < MM; j++) {
+    if (j < m) {
+      const int64_t v = b.v[j];
+      G |= (uint32_t)(sgn > 0 ? (v >= kRadix) : (v < 0)) << j;
+      P |= (uint32_t)(sgn > 0 ? (v == kMask) : (v == 0)) << j;
+    }
+  }
+  const uint32_t allp = (m >= 32) ? 0xffffffffu : ((1u << m) - 1u);
+  auto local = [&](uint32_t cin) -> uint64_t {
+    const uint64_t A = ((uint64_t)G << 1) | cin;
+    const uint64_t S = (A & P) + P;
+    return (S ^ P) | A;
+  };
+  const uint64_t C0 = local(0);
+  const uint32_t Gl = __ballot_sync(full, (C0 >> m) & 1);
+  const uint32_t Pl = __ballot_sync(full, P == allp);
+  // warp-level generate / propagate (carry-in 0)
+  {
+    const uint64_t A = ((uint64_t)Gl << 1) & 0xffffffffull;
+    const uint64_t S = (A & Pl) + Pl;
+    const int wgen = (int)(((S >> 32) & 1) | ((Gl >> 31) & 1));
+    if (lane == 0) {
+      xs[2 * gw] = wgen;
+      xs[2 * gw + 1] = (Pl == full) ? 1 : 0;
+    }
+  }
+  group_sync(bar_id, 32 * NW);
+  int wcin = 0;
+  for (int w = 0; w < gw; w++) wcin = (int)xs[2 * w] | ((int)xs[2 * w + 1] & wcin);
+  int gout = 0;  // carry leaving the last warp
+  {
+    int cc = 0;
+    for (int w = 0; w < NW; w++) cc = (int)xs[2 * w] | ((int)xs[2 * w + 1] & cc);
+    gout = cc;
+  }
+  const uint64_t A = (((uint64_t)Gl << 1) | (uint64_t)wcin) & 0xffffffffull;
+  const uint64_t S = (A & Pl) + Pl;
+  const uint32_t Cin = ((uint32_t)S ^ Pl) | (uint32_t)A;
+  const uint64_t C = local((Cin >> lane) & 1);
+#pragma unroll
+  for (int j = 0; j < MM; j++) {
+    if (j < m) {
+      const int64_t cj = (C >> j) & 1;
+      const int64_t oj = ((G >> j) & 1) | (((P >> j) & 1) & cj);
+      b.v[j] += sgn > 0 ? (cj - kRadix * oj) : (kRadix * oj - cj);
+    }
+  }
+  group_sync(bar_id, 32 * NW);  // xs reused by the next step
+  return sgn * (int64_t)gout;
+}
+
+template <int MM>
+__device__ __forceinline__ bool group_normalize_t(const int64_t* col, int ncols, int drop, int W, int32_t* out,
+                                                  int gw, int NW, int bar_id, int64_t* xs) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int per = (ncols + 32 * NW - 1) / (32 * NW);  // m: columns per lane
+  const int m = per;
+  const int base = gw * 32 * m;
+  Blk<MM> b;
+#pragma unroll
+  for (int j = 0; j < MM; j++) {
+    const int c = base + lane * m + j;
+    b.v[j] = (j < m && c < ncols) ? col[c] : 0;
+    if (drop && c == drop - 1) b.v[j] += kRadix / 2;
+  }
+  int64_t top = 0;
+#pragma unroll
+  for (int rnd = 0; rnd < 3; rnd++) {
+    int64_t c[MM];
+    int64_t cout = 0;
+#pragma unroll
+    for (int j = 0; j < MM; j++) {
+      c[j] = 0;
+      if (j < m) {
+        const int64_t v = b.v[j];
+        const int64_t dg = v & kMask;
+        c[j] = (v - dg) >> kRadixBits;
+        b.v[j] = dg;
+        if (j == m - 1) cout = c[j];
+      }
+    }
+    int64_t cin = __shfl_up_sync(full, cout, 1);
+    const int64_t wout = __shfl_sync(full, cout, 31);
+    if (lane == 0) xs[2 * gw] = wout;
+    group_sync(bar_id, 32 * NW);
+    if (lane == 0) cin = gw > 0 ? xs[2 * (gw - 1)] : 0;
+    top += xs[2 * (NW - 1)];
+#pragma unroll
+    for (int j = MM - 1; j >= 1; j--)
+      if (j < m) b.v[j] += c[j - 1];
+    b.v[0] += cin;
+    group_sync(bar_id, 32 * NW);
+  }
+  top += grp_lookahead(b, m, 1, gw, NW, bar_id, xs);
+  top += grp_lookahead(b, m, -1, gw, NW, bar_id, xs);
+#pragma unroll
+  for (int j = 0; j < MM; j++)
+    if (base + lane * m + j < drop) b.v[j] = 0;
+  const bool neg = top < 0;  // uniform over the group
+  if (neg) {
+#pragma unroll
+    for (int j = 0; j < MM; j++) {
+      const int c = base + lane * m + j;
+      if (j < m && c >= drop) b.v[j] = kMask - b.v[j] + (c == drop ? 1 : 0);
+    }
+    top = -top - 1 + grp_lookahead(b, m, 1, gw, NW, bar_id, xs);
+  }
+  bool ovf = top != 0;
+#pragma unroll
+  for (int j = 0; j < MM; j++) {
+    const int c = base + lane * m + j;
+    if (j < m && c >= drop) {
+      const int d = c - drop;
+      const int32_t dig = (int32_t)b.v[j];
+      if (d < W)
+        out[d] = neg ? -dig : dig;
+      else if (dig)
+        ovf = true;
+    }
+  }
+  for (int d = 32 * NW * m - drop + gw * 32 + lane; d < W; d += 32 * NW) out[d] = 0;
+  ovf = __any_sync(full, ovf);
+  if (lane == 0) xs[2 * gw] = ovf ? 1 : 0;
+  group_sync(bar_id, 32 * NW);
+  bool any = false;
+  for (int w = 0; w < NW; w++) any |= xs[2 * w] != 0;
+  group_sync(bar_id, 32 * NW);
+  return any;
+}
+
+// group normalisation + bot/top info (+ optional rounding to prec bits by warp 0)
+static __device__ __noinline__ bool group_normalize(const int64_t* col, int ncols, int drop, int W, int32_t* out,
+                                             int2* info, int round_prec_bits, int gw, int NW, int bar_id,
+                                             int64_t* xs);
+
 __device__ inline void round_to_prec(int32_t* out, int W, int prec_bits, bool& ovf) {
   // lane-0 sequential: round the canonical digit vector to prec_bits
   // significant bits, ties to even (the reference's state precision).
@@ -339,6 +492,52 @@ __device__ __forceinline__ bool warp_normalize_upto(const int64_t* col, int ncol
   tp = __reduce_max_sync(full, tp);
   if (lane == 0) *info = make_int2(tp >= 0 ? bot : W, tp);
   __syncwarp();
+  return ovf;
+}
+
+static __device__ __noinline__ bool group_normalize(const int64_t* col, int ncols, int drop, int W, int32_t* out,
+                                             int2* info, int round_prec_bits, int gw, int NW, int bar_id,
+                                             int64_t* xs) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int m = (ncols + 32 * NW - 1) / (32 * NW);
+  bool ovf;
+  if (m <= 2)
+    ovf = group_normalize_t<2>(col, ncols, drop, W, out, gw, NW, bar_id, xs);
+  else if (m <= 4)
+    ovf = group_normalize_t<4>(col, ncols, drop, W, out, gw, NW, bar_id, xs);
+  else
+    ovf = group_normalize_t<8>(col, ncols, drop, W, out, gw, NW, bar_id, xs);
+  if (round_prec_bits > 0) {
+    group_sync(bar_id, 32 * NW);
+    if (gw == 0 && lane == 0) round_to_prec(out, W, round_prec_bits, ovf);
+    if (gw == 0 && lane == 0) xs[0] = ovf ? 1 : 0;
+    group_sync(bar_id, 32 * NW);
+    ovf = xs[0] != 0;
+    group_sync(bar_id, 32 * NW);
+  }
+  int bot = 1 << 30, tp = -1;
+  for (int d = gw * 32 + lane; d < W; d += 32 * NW)
+    if (out[d]) {
+      bot = min(bot, d);
+      tp = max(tp, d);
+    }
+  bot = __reduce_min_sync(full, bot);
+  tp = __reduce_max_sync(full, tp);
+  if (lane == 0) {
+    xs[2 * gw] = bot;
+    xs[2 * gw + 1] = tp;
+  }
+  group_sync(bar_id, 32 * NW);
+  if (gw == 0 && lane == 0) {
+    int B0 = 1 << 30, T0 = -1;
+    for (int w = 0; w < NW; w++) {
+      B0 = min(B0, (int)xs[2 * w]);
+      T0 = max(T0, (int)xs[2 * w + 1]);
+    }
+    *info = make_int2(T0 >= 0 ? B0 : W, T0);
+  }
+  group_sync(bar_id, 32 * NW);
   return ovf;
 }
 

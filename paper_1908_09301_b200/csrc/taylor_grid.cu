@@ -52,7 +52,7 @@ __host__ __device__ inline Geo make_geo(const Params& p) {
 
 struct Layout {
   int rw, kc, nrows, nunits, ngmax, ncrow;
-  size_t off_stage, off_sinfo, off_crow, off_cinfo, off_part, off_pcar, off_cols, off_ssum, off_flag, total;
+  size_t off_stage, off_sinfo, off_crow, off_cinfo, off_part, off_pcar, off_cols, off_ssum, off_xs, off_flag, total;
 };
 
 // crow: cst D | lin D*D | q NT | ctab | U D | CUR D
@@ -64,7 +64,7 @@ __host__ __device__ inline Layout make_layout(const Params& p, int kc) {
   L.nrows = p.nlv + p.nrv;
   L.ncrow = p.D + p.D * p.D + p.NT + 1 + 2 * p.D;
   const int ns = kThreads / g.NGb > 0 ? kThreads / g.NGb : 1;
-  int nu = ns * (p.NP > 0 ? p.NP : 1) + p.D * p.D;
+  int nu = ns * (p.NP > 0 ? p.NP : 1) + 4 * p.D * p.D;
   if (p.D * kPC > nu) nu = p.D * kPC;
   L.nunits = nu;
   L.ngmax = g.NGb;
@@ -82,6 +82,7 @@ __host__ __device__ inline Layout make_layout(const Params& p, int kc) {
   L.off_pcar = take(sizeof(int64_t) * (size_t)nu * L.ngmax);
   L.off_cols = take(sizeof(int64_t) * (size_t)(p.NP + 2 * p.D) * g.NCX);
   L.off_ssum = take(sizeof(int64_t) * (size_t)p.D * (p.W + 3));
+  L.off_xs = take(sizeof(int64_t) * 4 * 64);
   L.off_flag = take(sizeof(int) * 8);
   L.total = o;
   return L;
@@ -163,6 +164,14 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
   int64_t* cols = (int64_t*)(smem + L.off_cols);
   int64_t* ssum = (int64_t*)(smem + L.off_ssum);
   int* flag = (int*)(smem + L.off_flag);
+  int64_t* xsb = (int64_t*)(smem + L.off_xs);
+  // normalisations: kNW warps per equation (named barrier 1 + m)
+  constexpr int kNW = 4;
+  const int geq = warp / kNW, gw = warp % kNW;
+  auto norm_eq = [&](int m, const int64_t* col, int ncol, int drop, int32_t* out, int2* info, int prec) {
+    if (group_normalize(col, ncol, drop, p.W, out, info, prec, gw, kNW, 1 + m, xsb + 64 * m) && gw == 0 && lane == 0)
+      flag[0] = 1;
+  };
   const int CR_LIN = p.D, CR_Q = CR_LIN + p.D * p.D, CR_CT = CR_Q + p.NT, CR_U = CR_CT + 1, CR_CUR = CR_U + p.D;
   auto CROW = [&](int r) { return crow + (size_t)r * rw; };
   auto SROW = [&](int r) { return stage + (size_t)r * rw; };
@@ -289,8 +298,11 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
       TSTAMP(1);
       // non-integer linear products: item it -> CTA it % nb
       const int nu_a = ns * p.NP;
-      for (int e = tid; e < nlin * g.NGb; e += kThreads) {
-        const int it = e / g.NGb, grp2 = e - it * g.NGb;
+      // (units nu_a + it*kLinPC + pc: one product split over kLinPC p-chunks)
+      constexpr int kLinPC = 4;
+      for (int e = tid; e < nlin * g.NGb * kLinPC; e += kThreads) {
+        const int it = e / (g.NGb * kLinPC), rem = e - it * g.NGb * kLinPC, grp2 = rem / kLinPC,
+                  pc = rem - grp2 * kLinPC;
         if (p.lin_small[it]) continue;
         const int j = it % p.D;
         const int c0 = kR * (g.gfb + grp2);
@@ -298,10 +310,11 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
         acc_zero(acc);
         if ((it % nb) == b && cinfo[CR_LIN + it].y >= 0) {
           int cnt = 0;
-          mac_group(acc, cnt, CROW(CR_LIN + it), cinfo[CR_LIN + it], CROW(CR_CUR + j), cinfo[CR_CUR + j], c0, g.Tb, mc);
+          mac_group_chunk(acc, cnt, CROW(CR_LIN + it), cinfo[CR_LIN + it], CROW(CR_CUR + j), cinfo[CR_CUR + j], c0,
+                          g.Tb, pc, kLinPC, mc);
           acc_fold(acc, c0, g.Tb);
         }
-        const int u = nu_a + it;
+        const int u = nu_a + it * kLinPC + pc;
         store_unit(part + (size_t)u * g.NCX, pcar + (size_t)u * L.ngmax, acc, grp2, c0, g.Tb);
       }
       __syncthreads();
@@ -318,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
                    unit_col(part, pcar, p.tpair[t], p.NP, nsa, g.NCX, L.ngmax, c, g.Tb, g.gfb, g.NGb);
         for (int j = 0; j < p.D; j++)
           if (!p.lin_small[m * p.D + j] && ((m * p.D + j) % nb) == b)
-            s += unit_col(part, pcar, nu_a + m * p.D + j, 1, 1, g.NCX, L.ngmax, c, g.Tb, g.gfb, g.NGb);
+            s += unit_col(part, pcar, nu_a + (m * p.D + j) * 4, 1, 4, g.NCX, L.ngmax, c, g.Tb, g.gfb, g.NGb);
         if (s != 0) atomicAdd(&ua[(size_t)m * g.NCX + c], (unsigned long long)s);
       }
       TSTAMP(2);
@@ -349,10 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
       }
       __syncthreads();
       TSTAMP(4);
-      for (int m = warp; m < p.D; m += nwarps)
-        if (warp_normalize(ucol + (size_t)m * g.NCX, g.ncolb, 2, p.W, CROW(CR_U + m), &cinfo[CR_U + m], 0) &&
-            lane == 0)
-          flag[0] = 1;
+      if (geq < p.D) norm_eq(geq, ucol + (size_t)geq * g.NCX, g.ncolb, 2, CROW(CR_U + geq), &cinfo[CR_U + geq], 0);
       if (warp == nwarps - 1) {
         const int2 inf = row_info_warp(CROW(CR_CT), p.W);
         if (lane == 0) cinfo[CR_CT] = inf;
@@ -406,10 +416,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
         ccol[(size_t)m * g.NCX + c] = (int64_t)__ldcg(&ca[(size_t)m * g.NCX + c]);
       }
       __syncthreads();
-      for (int m = warp; m < p.D; m += nwarps)
-        if (warp_normalize(ccol + (size_t)m * g.NCX, g.ncolc, 2, p.W, CROW(CR_CUR + m), &cinfo[CR_CUR + m], 0) &&
-            lane == 0)
-          flag[0] = 1;
+      if (geq < p.D) norm_eq(geq, ccol + (size_t)geq * g.NCX, g.ncolc, 2, CROW(CR_CUR + geq), &cinfo[CR_CUR + geq], 0);
       __syncthreads();
       TSTAMP(8);
       for (int m = warp; m < p.D; m += nwarps) {
@@ -424,10 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
 #undef TSTAMP
     }
     // state = RN_P(sum of the rows)
-    for (int m = warp; m < p.D; m += nwarps)
-      if (warp_normalize(ssum + (size_t)m * (p.W + 3), p.W + 3, 0, p.W, CROW(CR_CUR + m), &cinfo[CR_CUR + m], p.P) &&
-          lane == 0)
-        flag[0] = 1;
+    if (geq < p.D) norm_eq(geq, ssum + (size_t)geq * (p.W + 3), p.W + 3, 0, CROW(CR_CUR + geq), &cinfo[CR_CUR + geq], p.P);
     __syncthreads();
     if (b == 0 && ((n % p.stride == 0) || (n == p.n_steps))) {
       const int slot2 = (n % p.stride == 0) ? (n / p.stride - p.start_step / p.stride)

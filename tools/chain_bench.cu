@@ -67,7 +67,7 @@ __global__ void k(int W, long long* out) {
   for (int it = 0; it < 10; it++)
     warp_product(A + 16, make_int2(0, W - 1), B + 16, make_int2(0, W - 1), T, gf, ng, ncol, ncx, wsc, wcar, cols);
   long long t1 = clock64();
-  for (int it = 0; it < 10; it++) warp_normalize_small(cols, ncol, 2, W, res, &info, 0);
+  for (int it = 0; it < 10; it++) warp_normalize(cols, ncol, 2, W, res, &info, 0);
   long long t2 = clock64();
   if (lane == 0) {
     out[0] = (t1 - t0) / 10;
