@@ -506,8 +506,10 @@ static __device__ __noinline__ bool group_normalize(const int64_t* col, int ncol
     ovf = group_normalize_t<2>(col, ncols, drop, W, out, gw, NW, bar_id, xs);
   else if (m <= 4)
     ovf = group_normalize_t<4>(col, ncols, drop, W, out, gw, NW, bar_id, xs);
-  else
+  else if (m <= 8)
     ovf = group_normalize_t<8>(col, ncols, drop, W, out, gw, NW, bar_id, xs);
+  else
+    ovf = group_normalize_t<16>(col, ncols, drop, W, out, gw, NW, bar_id, xs);
   if (round_prec_bits > 0) {
     group_sync(bar_id, 32 * NW);
     if (gw == 0 && lane == 0) round_to_prec(out, W, round_prec_bits, ovf);

@@ -55,6 +55,15 @@ struct Layout {
   size_t off_stage, off_sinfo, off_crow, off_cinfo, off_part, off_pcar, off_cols, off_ssum, off_xs, off_flag, total;
 };
 
+// non-integer linear coefficients get kLinPC partial units each, packed in
+// order of appearance (slot = count of non-small entries before it)
+constexpr int kLinPC = 4;
+__host__ __device__ inline int lin_slot(const Params& p, int it) {
+  int s = 0;
+  for (int t = 0; t < it; t++) s += p.lin_small[t] ? 0 : 1;
+  return s;
+}
+
 // crow: cst D | lin D*D | q NT | ctab | U D | CUR D
 __host__ __device__ inline Layout make_layout(const Params& p, int kc) {
   Layout L;
@@ -64,7 +73,7 @@ __host__ __device__ inline Layout make_layout(const Params& p, int kc) {
   L.nrows = p.nlv + p.nrv;
   L.ncrow = p.D + p.D * p.D + p.NT + 1 + 2 * p.D;
   const int ns = kThreads / g.NGb > 0 ? kThreads / g.NGb : 1;
-  int nu = ns * (p.NP > 0 ? p.NP : 1) + 4 * p.D * p.D;
+  int nu = ns * (p.NP > 0 ? p.NP : 1) + kLinPC * lin_slot(p, p.D * p.D);
   if (p.D * kPC > nu) nu = p.D * kPC;
   L.nunits = nu;
   L.ngmax = g.NGb;
@@ -82,7 +91,7 @@ __host__ __device__ inline Layout make_layout(const Params& p, int kc) {
   L.off_pcar = take(sizeof(int64_t) * (size_t)nu * L.ngmax);
   L.off_cols = take(sizeof(int64_t) * (size_t)(p.NP + 2 * p.D) * g.NCX);
   L.off_ssum = take(sizeof(int64_t) * (size_t)p.D * (p.W + 3));
-  L.off_xs = take(sizeof(int64_t) * 4 * 64);
+  L.off_xs = take(sizeof(int64_t) * kMaxD * 32);
   L.off_flag = take(sizeof(int) * 8);
   L.total = o;
   return L;
@@ -169,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
   constexpr int kNW = 4;
   const int geq = warp / kNW, gw = warp % kNW;
   auto norm_eq = [&](int m, const int64_t* col, int ncol, int drop, int32_t* out, int2* info, int prec) {
-    if (group_normalize(col, ncol, drop, p.W, out, info, prec, gw, kNW, 1 + m, xsb + 64 * m) && gw == 0 && lane == 0)
+    if (group_normalize(col, ncol, drop, p.W, out, info, prec, gw, kNW, 1 + m, xsb + 32 * m) && gw == 0 && lane == 0)
       flag[0] = 1;
   };
   const int CR_LIN = p.D, CR_Q = CR_LIN + p.D * p.D, CR_CT = CR_Q + p.NT, CR_U = CR_CT + 1, CR_CUR = CR_U + p.D;
@@ -298,8 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
       TSTAMP(1);
       // non-integer linear products: item it -> CTA it % nb
       const int nu_a = ns * p.NP;
-      // (units nu_a + it*kLinPC + pc: one product split over kLinPC p-chunks)
-      constexpr int kLinPC = 4;
+      // (units nu_a + slot*kLinPC + pc: one product split over kLinPC p-chunks)
       for (int e = tid; e < nlin * g.NGb * kLinPC; e += kThreads) {
         const int it = e / (g.NGb * kLinPC), rem = e - it * g.NGb * kLinPC, grp2 = rem / kLinPC,
                   pc = rem - grp2 * kLinPC;
@@ -314,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
                           g.Tb, pc, kLinPC, mc);
           acc_fold(acc, c0, g.Tb);
         }
-        const int u = nu_a + it * kLinPC + pc;
+        const int u = nu_a + lin_slot(p, it) * kLinPC + pc;
         store_unit(part + (size_t)u * g.NCX, pcar + (size_t)u * L.ngmax, acc, grp2, c0, g.Tb);
       }
       __syncthreads();
@@ -331,7 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
                    unit_col(part, pcar, p.tpair[t], p.NP, nsa, g.NCX, L.ngmax, c, g.Tb, g.gfb, g.NGb);
         for (int j = 0; j < p.D; j++)
           if (!p.lin_small[m * p.D + j] && ((m * p.D + j) % nb) == b)
-            s += unit_col(part, pcar, nu_a + (m * p.D + j) * 4, 1, 4, g.NCX, L.ngmax, c, g.Tb, g.gfb, g.NGb);
+            s += unit_col(part, pcar, nu_a + lin_slot(p, m * p.D + j) * kLinPC, 1, kLinPC, g.NCX, L.ngmax, c, g.Tb, g.gfb, g.NGb);
         if (s != 0) atomicAdd(&ua[(size_t)m * g.NCX + c], (unsigned long long)s);
       }
       TSTAMP(2);
