@@ -144,6 +144,46 @@ def test_dropin_integrate_matches_reference(golden, gpu, name):
         assert d == EXACT or d >= K - guard_digits(pt.step * tau), (name, pt.step, d)
 
 
+LONG_RUNS = ("config1_k500_n200_10000", "config2_k2200_n1000_500", "config3_k4200_n3500_4")
+
+
+@pytest.mark.parametrize("name", LONG_RUNS)
+def test_long_run_agreement_vs_oracle(gpu, name):
+    """BASELINE.json configs 1-3 at full size, through the drop-in entry point,
+    against the oracle's frozen trajectories (tests/golden/oracle_*.json: the
+    reference algorithm on MPFR, bit-pinned to the reference by
+    make_golden.py).  Every recorded output time must agree to 10^-(K-d(t));
+    the agreement per record is written to gpurun_out/parity_<name>.json."""
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(__file__), "golden", f"oracle_{name}.json")
+    with open(path) as fh:
+        c = json.load(fh)
+    P = c["prec_bits"]
+    ctx = M.PrecisionContext(P)
+    system = M.builtin_system("lorenz", ctx)
+    state0 = tuple(M.mp_from_decimal(t, ctx) for t in c["init"])
+    traj = M.integrate(system, state0, M.StepConfig(c["tau"], c["order"]), c["n_steps"], ctx,
+                       record_stride=c["stride"])
+    assert traj.steps() == [r["step"] for r in c["records"]]
+    K = c["K"]
+    tau = abs(float(Fraction(c["tau"])))
+    report = []
+    for pt, rec in zip(traj.points, c["records"]):
+        got = [v.as_fraction() for v in pt.state]
+        ref = [frac(h) for h in rec["state"]]
+        d = agreement_digits(got, ref)
+        need = K - guard_digits(pt.step * tau)
+        report.append({"step": pt.step, "t": pt.step * tau, "agree_digits": None if d == EXACT else d,
+                       "required": need})
+        assert d == EXACT or d >= need, (name, pt.step, d, need)
+    out = os.path.join(os.environ.get("GRAFT_REPO_ROOT", "."), "gpurun_out")
+    os.makedirs(out, exist_ok=True)
+    with open(os.path.join(out, f"parity_{name}.json"), "w") as fh:
+        json.dump({"name": name, "K": K, "prec_bits": P, "order": c["order"], "records": report}, fh, indent=1)
+
+
 def test_reference_regression_pair_on_gpu(gpu):
     """The reference's frozen agreement series (tests/test_cns.py:105), from GPU runs."""
     runs = {}
