@@ -10,13 +10,16 @@
  * (/root/reference/pkg/src/mptaylor):
  *
  *   mpt_plan_create / mpt_plan_set_constants
- *       the per-run setup the reference does in taylor.py:224 integrate
- *       (tau = cfg.tau(ctx), pairs = system.product_pairs(), systems.py:64)
- *       and in reduction.py:174 SerialReducer / ProcessReducer construction.
- *   mpt_integrate            taylor.py:224 integrate  (host buffers in/out)
+ *       the per-run setup the reference does in taylor.py:202 integrate
+ *       (tau = cfg.tau(ctx) at :234, pairs = system.product_pairs() at :239,
+ *       systems.py:65) and in reduction.py:187 SerialReducer / :279 ProcessReducer
+ *       construction (the coefficient recurrence's session state).
+ *   mpt_integrate            taylor.py:202 integrate  (host buffers in/out; the
+ *                            stepping loop :242-253, _jet_rows :117, the Cauchy sums
+ *                            reduction.py:149 convolve, horner_eval :168)
  *   mpt_integrate_device     the same on device-resident state (no copies)
- *   mpt_compute_jet          taylor.py:167 compute_jet (one jet per trajectory)
- *   mpt_step                 taylor.py:204 step       (n_steps = 1, no records)
+ *   mpt_compute_jet          taylor.py:139 compute_jet (one jet per trajectory)
+ *   mpt_step                 taylor.py:182 step       (n_steps = 1, no records)
  *
  * All functions return 0 on success and a negative code on failure; the
  * message is available from mpt_last_error(). There is no CPU fallback: if no
@@ -61,9 +64,10 @@ int mpt_plan_create(mpt_plan **plan, int dim, int nterms, const int32_t *term_eq
                     int order, int prec_bits, int n_traj, int device);
 int mpt_plan_destroy(mpt_plan *plan);
 
-/* Kernel selection (default: automatic -- the shared-memory-resident cluster
- * kernel when the coefficient rows fit, with an 8-CTA cluster per trajectory
- * for single-trajectory plans; otherwise the team kernel with rows in HBM).
+/* Kernel selection (default: automatic -- single trajectories use the
+ * pipelined cluster kernel (rows resident in distributed smem, up to 16 CTAs)
+ * when the system fits it, else the cluster kernel, else the grid kernel on all
+ * SMs; ensembles use the team kernel, one CTA per trajectory).
  * kernel: 0 auto, 1 team (rows in HBM/L2), 2 cluster (rows in smem),
  *         3 pipelined cluster kernel (warp-specialised lookahead, single trajectories),
  *         4 grid kernel (one trajectory on every SM, rows in L2; large precision);

@@ -27,8 +27,8 @@
  *                 rounding to the reference precision P)
  *
  * Terms are grouped by equation in stored order like the reference's
- * systems.py:31 QuadraticODESystem; pairs are distinct (j,k) in first
- * appearance order (systems.py:64 product_pairs).
+ * systems.py:32 QuadraticODESystem; pairs are distinct (j,k) in first
+ * appearance order (systems.py:65 product_pairs).
  */
 #include <stdint.h>
 #include <stdlib.h>

@@ -7,17 +7,17 @@
  * product path (paper_1908_09301_b200) never links or calls this file.
  *
  * What it restates (reference = /root/reference/pkg/src/mptaylor):
- *   taylor.py:148 _jet_rows        order loop, frozen evaluation order:
+ *   taylor.py:117 _jet_rows        order loop, frozen evaluation order:
  *                                  constant (i==0 only), linear terms in
  *                                  ascending j, bilinear terms in stored order,
  *                                  then one multiply by inv = div(1, i+1).
- *   reduction.py:96  _fold_chunk    ascending-k fold, one rounding per mul/add,
+ *   reduction.py:93  _fold_chunk    ascending-k fold, one rounding per mul/add,
  *                                  all product pairs fused in one pass.
- *   reduction.py:121 _merge_partials ascending chunk order, empty chunks skipped.
- *   reduction.py:131 _convolve_value serial fold below threshold / 1 chunk,
- *                                  else chunk_bounds partition (reduction.py:88).
- *   taylor.py:187 horner_eval       acc = a[N]; acc = add(a[idx], mul(tau, acc)).
- *   taylor.py:224 integrate         one jet per step, record every stride +
+ *   reduction.py:126 _merge_partials ascending chunk order, empty chunks skipped.
+ *   reduction.py:136 _convolve_value serial fold below threshold / 1 chunk,
+ *                                  else chunk_bounds partition (reduction.py:84).
+ *   taylor.py:168 horner_eval       acc = a[N]; acc = add(a[idx], mul(tau, acc)).
+ *   taylor.py:202 integrate         one jet per step, record every stride +
  *                                  final step, absolute stride grid on resume.
  * Every operation is an MPFR call with MPFR_RNDN at the context precision,
  * which is exactly what gmpy2's context methods do for the reference.
@@ -86,7 +86,7 @@ typedef struct {
   mpfr_t *linear;   /* dim*dim, row m = equation m */
   mpfr_t *tcoef;    /* nterms, grouped by equation in stored order */
   int *teq, *tj, *tk, *tpair;
-  int *pj, *pk; /* distinct (j,k) in first-appearance order: systems.py:64 product_pairs */
+  int *pj, *pk; /* distinct (j,k) in first-appearance order: systems.py:65 product_pairs */
 } sys_t;
 
 static void sys_free(sys_t *s) {
@@ -140,7 +140,7 @@ static void sys_build(sys_t *s, int prec, int dim, int nterms, const int32_t *te
   }
 }
 
-/* reduction.py:88 chunk_bounds */
+/* reduction.py:84 chunk_bounds */
 static void chunk_bounds(int i, int nchunks, int c, int *lo, int *hi) {
   int total = i + 1;
   int base = total / nchunks, rem = total % nchunks;
@@ -156,7 +156,7 @@ typedef struct {
 
 #define COEF(J, m, i) ((J)->coef[(size_t)(m) * ((J)->order + 1) + (i)])
 
-/* reduction.py:96 _fold_chunk for every pair, k in [lo, hi] */
+/* reduction.py:93 _fold_chunk for every pair, k in [lo, hi] */
 static void fold_chunk(const sys_t *s, jet_t *J, int i, int lo, int hi, mpfr_t *sums, mpfr_ptr tmp) {
   for (int p = 0; p < s->npairs; p++)
     mpfr_mul(sums[p], COEF(J, s->pj[p], i - lo), COEF(J, s->pk[p], lo), RND);
@@ -174,7 +174,7 @@ typedef struct {
   mpfr_t *tmp;  /* nchunks */
 } red_t;
 
-/* reduction.py:131 _convolve_value */
+/* reduction.py:136 _convolve_value */
 static void convolve_value(const sys_t *s, jet_t *J, int i, red_t *R, mpfr_t *sums, mpfr_ptr tmp) {
   int c_eff = R->nchunks;
   if (i + 1 < R->threshold || c_eff == 1) {
@@ -203,7 +203,7 @@ static void convolve_value(const sys_t *s, jet_t *J, int i, red_t *R, mpfr_t *su
   }
 }
 
-/* taylor.py:148 _jet_rows; J->coef[m][0] must hold the state */
+/* taylor.py:117 _jet_rows; J->coef[m][0] must hold the state */
 static void jet_rows(const sys_t *s, jet_t *J, red_t *R, mpfr_t *sums, mpfr_ptr tmp, mpfr_ptr acc,
                      mpfr_ptr inv, mpfr_ptr one) {
   int dim = s->dim;
@@ -235,7 +235,7 @@ static void jet_rows(const sys_t *s, jet_t *J, red_t *R, mpfr_t *sums, mpfr_ptr 
   }
 }
 
-/* taylor.py:187 horner_eval */
+/* taylor.py:168 horner_eval */
 static void horner(jet_t *J, int m, mpfr_srcptr tau, mpfr_ptr out, mpfr_ptr tmp) {
   int n = J->order;
   if (mpfr_zero_p(tau)) {
@@ -302,7 +302,7 @@ static void run_free(run_t *r) {
 const char *ref_mpfr_version(void) { return mpfr_get_version(); }
 
 /*
- * One jet (taylor.py:167 compute_jet). Inputs packed as
+ * One jet (taylor.py:139 compute_jet). Inputs packed as
  * [constants(dim), linear(dim*dim), term coefs(nterms), state(dim)].
  * Output: dim*(order+1) values, row-major by variable.
  */
@@ -327,10 +327,10 @@ int ref_compute_jet(int prec, int dim, int nterms, const int32_t *teq, const int
 }
 
 /*
- * taylor.py:224 integrate. Inputs packed as
+ * taylor.py:202 integrate. Inputs packed as
  * [constants(dim), linear(dim*dim), term coefs(nterms), state0(dim), tau].
  * Records (step, state) for step start_step, every multiple of stride, and
- * n_steps (taylor.py:217 _record_steps); returns the number of records or a
+ * n_steps (taylor.py:195 _record_steps); returns the number of records or a
  * negative error (-1 mantissa overflow, -2 record buffer too small).
  */
 int ref_integrate(int prec, int dim, int nterms, const int32_t *teq, const int32_t *tj,
@@ -367,7 +367,7 @@ done:
   return rc < 0 ? rc : nrec;
 }
 
-/* reduction.py:162 convolve / convolve_pair (npairs = 1 or 2 arrays pairs) */
+/* reduction.py:149 convolve / convolve_pair (npairs = 1 or 2 arrays pairs) */
 int ref_convolve(int prec, int npairs, int len, const int32_t *sgn, const int64_t *ex,
                  const uint64_t *limbs, int nl, int i, int nchunks, int threshold, int nthreads,
                  int32_t *osgn, int64_t *oex, uint64_t *olimbs, int onl) {
@@ -412,7 +412,7 @@ int ref_convolve(int prec, int npairs, int len, const int32_t *sgn, const int64_
   return rc;
 }
 
-/* ---- conversion helpers (mp.py:118 mp_from_decimal, systems.py:91 div(8,3)) ---- */
+/* ---- conversion helpers (mp.py:122 mp_from_decimal, systems.py:90 div(8,3)) ---- */
 int mpfr_set_str(mpfr_ptr, const char *, int, mpfr_rnd_t);
 
 /* RN_prec of a decimal literal; 0 ok, -1 parse error */

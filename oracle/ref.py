@@ -8,7 +8,7 @@ has no route into this module.
 Values are exact dyadics ``Dy(sign, mant, exp)`` = sign * mant * 2**exp,
 sign in {+1, -1} (kept for zeros so -0 survives), mant >= 0. The system
 description mirrors the reference's QuadraticODESystem
-(/root/reference/pkg/src/mptaylor/systems.py:31): dense constant vector,
+(/root/reference/pkg/src/mptaylor/systems.py:32): dense constant vector,
 dense linear matrix, bilinear terms per equation in stored order.
 """
 
@@ -145,7 +145,7 @@ def _onl(prec):
 
 # ------------------------------------------------------------ conversions
 def from_decimal(text: str, prec: int) -> Dy:
-    """RN_prec of a decimal literal (mp.py:118 mp_from_decimal on MPFR)."""
+    """RN_prec of a decimal literal (mp.py:122 mp_from_decimal on MPFR)."""
     onl = _onl(prec)
     s, e, l = _out(1, onl)
     rc = lib().ref_from_decimal(prec, text.strip().encode(), s, e, l, onl)
@@ -183,7 +183,7 @@ def neg(v: Dy) -> Dy:
 
 # ---------------------------------------------------------------- systems
 def lorenz(prec: int, sigma=10, r=28, b_num=8, b_den=3):
-    """systems.py:107 lorenz_system with LorenzParams.default (systems.py:88)."""
+    """systems.py:94 lorenz_system with LorenzParams.default (systems.py:84)."""
     zero = Dy(1, 0, 0)
     one = from_int(1, prec)
     s = from_int(sigma, prec)
@@ -212,7 +212,7 @@ def _sys_pack(system, extra):
 
 
 def compute_jet(system, state, order, prec, chunks=64, threshold=256, threads=1):
-    """taylor.py:167 compute_jet -> coeffs[m][i] as Dy."""
+    """taylor.py:139 compute_jet -> coeffs[m][i] as Dy."""
     dim, nt, teq, tj, tk, sgn, ex, limbs, nl = _sys_pack(system, state)
     onl = _onl(prec)
     n = dim * (order + 1)
@@ -229,7 +229,7 @@ def compute_jet(system, state, order, prec, chunks=64, threshold=256, threads=1)
 
 def integrate(system, state0, tau, order, n_steps, prec, stride=100, start_step=0,
               chunks=64, threshold=256, threads=1):
-    """taylor.py:224 integrate -> [(step, [Dy]*dim)] on the reference's record grid."""
+    """taylor.py:202 integrate -> [(step, [Dy]*dim)] on the reference's record grid."""
     dim, nt, teq, tj, tk, sgn, ex, limbs, nl = _sys_pack(system, list(state0) + [tau])
     onl = _onl(prec)
     max_rec = (n_steps - start_step) // stride + 3
@@ -246,7 +246,7 @@ def integrate(system, state0, tau, order, n_steps, prec, stride=100, start_step=
 
 
 def convolve(arrays, i, prec, chunks=64, threshold=256, threads=1):
-    """reduction.py:162 convolve (2 arrays) / convolve_pair (4 arrays)."""
+    """reduction.py:149 convolve (2 arrays) / convolve_pair (4 arrays)."""
     npairs = len(arrays) // 2
     length = len(arrays[0])
     vals = [v for arr in arrays for v in arr]

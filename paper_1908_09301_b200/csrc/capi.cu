@@ -201,7 +201,7 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
   p.P = prec_bits;
   p.n_traj = n_traj;
   p.nthreads = 256;
-  // distinct pairs in first-appearance order (systems.py:64 product_pairs)
+  // distinct pairs in first-appearance order (systems.py:65 product_pairs)
   for (int t = 0; t < nterms; t++) {
     if (term_eq[t] < 0 || term_eq[t] >= dim || term_j[t] < 0 || term_k[t] < term_j[t] || term_k[t] >= dim) {
       delete pl;

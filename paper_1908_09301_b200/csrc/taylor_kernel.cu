@@ -2,7 +2,7 @@
 //
 // One CTA owns one trajectory for the whole launch: it loops over steps and,
 // inside each step, over the Taylor orders i = 0..N-1 of the recurrence
-// (reference taylor.py:148 _jet_rows, paper Eq. (3)), with __syncthreads()
+// (reference taylor.py:117 _jet_rows, paper Eq. (3)), with __syncthreads()
 // between phases instead of kernel relaunches. Per order:
 //
 //   phase A  Cauchy sums  S_p = sum_k coef[j_p][i-k] (x) coef[k_p][k]
@@ -14,7 +14,7 @@
 //   phase C  coef[m][i+1] = U_m (x) tau/(i+1)       (the 1/(i+1) scaling)
 //
 // and after the last order the state update x_{n+1} = sum_i coef[i] (the
-// tau-scaled Horner evaluation, reference taylor.py:187) followed by the
+// tau-scaled Horner evaluation, reference taylor.py:168) followed by the
 // rounding of the state to the reference precision P (round-to-nearest-even).
 // oracle/fixmodel.c restates exactly this arithmetic on the CPU.
 #include <cuda_runtime.h>

@@ -2,9 +2,9 @@
 bound to device buffers through the C ABI (include/mptaylor_b200.h).
 
 A plan replaces, for one (system, precision, order, tau) tuple, everything
-the reference builds per call of taylor.py:224 integrate / :167 compute_jet:
-the product-pair list (systems.py:64), the reducer session
-(reduction.py:174/:262) and the per-order 1/(i+1) factors (taylor.py:152),
+the reference builds per call of taylor.py:202 integrate / :139 compute_jet:
+the product-pair list (systems.py:65), the reducer session
+(reduction.py:187/:279) and the per-order 1/(i+1) factors (taylor.py:125),
 which here become the tau/(i+1) table of the tau-scaled recurrence.
 """
 
@@ -142,7 +142,7 @@ class DevicePlan:
         out = np.zeros_like(st)
         status = np.zeros(self.n_traj, np.int32)
         _native.check(self.lib.mpt_step(self.h, _p(st), _p(out), _p(status)))
-        return out
+        return out, status
 
     # device-resident throughput path ------------------------------------
     def upload(self, state):

@@ -242,7 +242,7 @@ class PrecisionContext:
 
 
 def mp_from_decimal(text: str, ctx: PrecisionContext) -> MPValue:
-    """Parse a decimal string to the nearest representable value (mp.py:118)."""
+    """Parse a decimal string to the nearest representable value (mp.py:122)."""
     if not isinstance(text, str):
         raise ValueError(f"decimal text must be a string, got {type(text).__name__}")
     stripped = text.strip()
@@ -298,7 +298,7 @@ def _decimal_digits_of(f: Fraction, n: int):
 
 
 def mp_to_decimal(v: MPValue, digits: int) -> str:
-    """Correctly rounded decimal with `digits` significant digits (mp.py:144)."""
+    """Correctly rounded decimal with `digits` significant digits (mp.py:146)."""
     if not isinstance(digits, int) or isinstance(digits, bool) or digits < 1:
         raise ValueError(f"digits must be a positive integer, got {digits!r}")
     if v.is_zero():
@@ -323,14 +323,14 @@ _ARITH_OPS = ("add", "sub", "mul", "div")
 
 
 def arith(op: str, a: MPValue, b: MPValue, ctx: PrecisionContext) -> MPValue:
-    """One of add/sub/mul/div with a single rounding (mp.py:171)."""
+    """One of add/sub/mul/div with a single rounding (mp.py:178)."""
     if op not in _ARITH_OPS:
         raise ValueError(f"unknown operation {op!r}, expected one of {_ARITH_OPS}")
     return getattr(ctx, op)(a, b)
 
 
 def decimal_digits(precision_bits: int) -> int:
-    """floor(precision_bits * log10 2), exactly (mp.py:185)."""
+    """floor(precision_bits * log10 2), exactly (mp.py:189)."""
     if not isinstance(precision_bits, int) or isinstance(precision_bits, bool):
         raise TypeError(f"precision_bits must be an int, got {precision_bits!r}")
     if precision_bits < 1:
@@ -345,7 +345,7 @@ def decimal_digits(precision_bits: int) -> int:
 
 
 def bits_for_digits(digits: int) -> int:
-    """Smallest p with 2**p >= 10**digits (mp.py:205)."""
+    """Smallest p with 2**p >= 10**digits (mp.py:209)."""
     if not isinstance(digits, int) or isinstance(digits, bool):
         raise TypeError(f"digits must be an int, got {digits!r}")
     if digits < 1:
@@ -360,7 +360,7 @@ def bits_for_digits(digits: int) -> int:
 
 
 def mp_bits_equal(a: MPValue, b: MPValue) -> bool:
-    """Identical bit patterns, -0 != +0, precision must match (mp.py:226)."""
+    """Identical bit patterns, -0 != +0, precision must match (mp.py:229)."""
     if a.precision != b.precision:
         return False
     if a.is_zero() or b.is_zero():

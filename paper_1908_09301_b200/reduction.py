@@ -44,14 +44,14 @@ class ReducePlan:
 
 
 def chunk_bounds(i: int, num_chunks: int, c: int) -> tuple:
-    """Inclusive (lo, hi) of chunk c of [0, i] (reduction.py:88)."""
+    """Inclusive (lo, hi) of chunk c of [0, i] (reduction.py:84)."""
     base, rem = divmod(i + 1, num_chunks)
     lo = c * base + min(c, rem)
     return lo, lo + base + (1 if c < rem else 0) - 1
 
 
 def partition(i: int, num_chunks: int) -> list:
-    """[0, i] in num_chunks contiguous near-equal ranges, larger first (reduction.py:72)."""
+    """[0, i] in num_chunks contiguous near-equal ranges, larger first (reduction.py:70)."""
     if i < 0:
         raise ValueError(f"order index must be >= 0, got {i}")
     if num_chunks < 1:
@@ -61,7 +61,7 @@ def partition(i: int, num_chunks: int) -> list:
 
 class DeviceReducer:
     """Device options for the Taylor engine; a context manager like the
-    reference reducers (reduction.py:174 SerialReducer)."""
+    reference reducers (reduction.py:187 SerialReducer)."""
 
     def __init__(self, plan: ReducePlan | None = None, device: int = 0,
                  guard_bits: int = DEFAULT_GUARD_BITS):

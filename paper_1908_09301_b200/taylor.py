@@ -4,10 +4,10 @@ same names, signatures, recording policy, observer protocol and errors.
 
 What changes underneath:
   * numbers are device fixed-point digit rows with F >= P + guard bits;
-  * the coefficient recurrence (taylor.py:148) runs tau-scaled,
+  * the coefficient recurrence (taylor.py:117) runs tau-scaled,
     a~_{i+1} = tau/(i+1) * (...), in one persistent CUDA kernel per launch;
     the Cauchy sums are exact integer column sums rounded once;
-  * the Horner evaluation (taylor.py:187) becomes the exact sum of the
+  * the Horner evaluation (taylor.py:168) becomes the exact sum of the
     scaled rows, fused into the same kernel, and the state is rounded to the
     context precision P (round-to-nearest-even) after every step, so every
     recorded state is a P-bit MPValue like the reference's.
@@ -32,7 +32,7 @@ DEFAULT_RECORD_STRIDE = 100
 
 @dataclass(frozen=True)
 class Jet:
-    """coeffs[m][i] = i-th normalized derivative of variable m (taylor.py:33)."""
+    """coeffs[m][i] = i-th normalized derivative of variable m (taylor.py:37)."""
 
     dim: int
     order: int
@@ -47,7 +47,7 @@ class Jet:
 
 @dataclass(frozen=True)
 class StepConfig:
-    """Step size as exact decimal text, method order, workers (taylor.py:55)."""
+    """Step size as exact decimal text, method order, workers (taylor.py:57)."""
 
     tau_text: str
     order_n: int
@@ -77,7 +77,7 @@ class TrajectoryPoint:
 
 @dataclass
 class Trajectory:
-    """Recorded states sampled on a fixed step stride (taylor.py:96)."""
+    """Recorded states sampled on a fixed step stride (taylor.py:92)."""
 
     dim: int
     tau_text: str
@@ -94,7 +94,7 @@ class Trajectory:
 
 
 def exact_time(step: int, tau_text: str) -> Decimal:
-    """step * tau as an exact decimal (taylor.py:115)."""
+    """step * tau as an exact decimal (taylor.py:109)."""
     tau = Decimal(tau_text)
     with localcontext() as dctx:
         dctx.prec = len(tau.as_tuple().digits) + len(str(step)) + 4
@@ -117,7 +117,7 @@ def _check_state(system: QuadraticODESystem, state):
 
 
 def compute_jet(system: QuadraticODESystem, state, order_n: int, ctx: PrecisionContext, reducer=None) -> Jet:
-    """Taylor coefficients through `state` up to order_n (taylor.py:167).
+    """Taylor coefficients through `state` up to order_n (taylor.py:139).
 
     The device computes the jet scaled by s^i with s = 2^-k (exact power of
     two, so unscaling is exact); k grows until no coefficient leaves the
@@ -153,7 +153,7 @@ def compute_jet(system: QuadraticODESystem, state, order_n: int, ctx: PrecisionC
 
 
 def horner_eval(jet_row, tau: MPValue, ctx: PrecisionContext) -> MPValue:
-    """a[0] + tau*(a[1] + tau*(a[2] + ...)) (taylor.py:187).
+    """a[0] + tau*(a[1] + tau*(a[2] + ...)) (taylor.py:168).
 
     A host utility on MPValues for API completeness; the stepping path never
     calls it (its evaluation is fused into the device kernel)."""
@@ -176,11 +176,14 @@ def _plan_for(system, cfg: StepConfig, ctx: PrecisionContext, reducer, n_traj=1)
 
 
 def step(system: QuadraticODESystem, state, cfg: StepConfig, ctx: PrecisionContext, reducer=None) -> tuple:
-    """Advance the state by one Taylor step of size cfg.tau (taylor.py:204)."""
+    """Advance the state by one Taylor step of size cfg.tau (taylor.py:182)."""
     _check_state(system, state)
     fmt, plan = _plan_for(system, cfg, ctx, reducer)
     with plan:
-        out = plan.step(fmt.to_digits(state))[0]
+        out, status = plan.step(fmt.to_digits(state))
+    if status.any():
+        raise RangeError("state left the device fixed-point range (|x| >= 2^27) in step")
+    out = out[0]
     return _to_values(fmt, out, ctx.precision_bits)
 
 
@@ -195,7 +198,7 @@ def integrate(
     record_stride: int = DEFAULT_RECORD_STRIDE,
     start_step: int = 0,
 ) -> Trajectory:
-    """Apply `step` n_steps times on the device (taylor.py:224).
+    """Apply `step` n_steps times on the device (taylor.py:202).
 
     Records step start_step, every multiple of record_stride and n_steps; an
     observer, when given, is called once per step with (n, exact time,
@@ -215,7 +218,9 @@ def integrate(
     fmt, plan = _plan_for(system, cfg, ctx, reducer)
     dev_stride = 1 if observer is not None else record_stride
     with plan:
-        steps, recs, _ = plan.integrate(fmt.to_digits(state0), n_steps, start_step, dev_stride)
+        steps, recs, status = plan.integrate(fmt.to_digits(state0), n_steps, start_step, dev_stride)
+    if status.any():
+        raise RangeError("state left the device fixed-point range (|x| >= 2^27) during integrate")
     prec = ctx.precision_bits
     for r in range(1, len(steps)):
         n = int(steps[r])

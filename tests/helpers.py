@@ -25,7 +25,7 @@ def floor_neg_log10(rel: Fraction) -> int:
 
 
 def agreement_digits(a, b) -> float:
-    """The reference's coincidence metric (cns.py:56 agreement_digits):
+    """The reference's coincidence metric (cns.py:52 agreement_digits):
     min over components of floor(-log10(|a-b| / max(|a|, |b|, 1))), EXACT
     when all components are identical."""
     worst = None

@@ -185,7 +185,7 @@ def test_long_run_agreement_vs_oracle(gpu, name):
 
 
 def test_reference_regression_pair_on_gpu(gpu):
-    """The reference's frozen agreement series (tests/test_cns.py:105), from GPU runs."""
+    """The reference's frozen agreement series (tests/test_cns.py:119), from GPU runs."""
     runs = {}
     for P, N in ((128, 20), (256, 30)):
         ctx = M.PrecisionContext(P)

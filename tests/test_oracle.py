@@ -6,7 +6,7 @@ against the C oracle. These tests re-establish the pin on every run (no
 /root/reference needed) and check the reference's own known answers:
 hand-derived coefficients (test_acceptance.py criterion 1), e within 1e-32
 (criterion 2) and the frozen agreement series of the 128/256-bit pair
-(test_cns.py:105: 38 digits at t=0, 23 at t=1, 13 at t=25, t_c = 25).
+(test_cns.py:119: 38 digits at t=0, 23 at t=1, 13 at t=25, t_c = 25).
 """
 
 from fractions import Fraction
