@@ -89,13 +89,28 @@ class FixedFormat:
         return out
 
     def digits_to_ints(self, rows) -> list:
+        """Digit rows -> integers. Canonical rows (every digit carries the
+        value's sign) are packed through their bit patterns (vectorised);
+        other rows take the exact digit-by-digit path."""
         rows = np.asarray(rows, dtype=np.int64).reshape(-1, self.width)
+        if rows.shape[0] == 0:
+            return []
+        neg = (rows < 0).any(axis=1)
+        canon = ~(neg & (rows > 0).any(axis=1)) & (np.abs(rows) < (1 << RADIX_BITS)).all(axis=1)
+        mags = np.abs(rows).astype("<u4")
+        bits = np.unpackbits(mags.view(np.uint8).reshape(rows.shape[0], self.width, 4), axis=2,
+                             bitorder="little")[:, :, :RADIX_BITS].reshape(rows.shape[0], -1)
+        packed = np.packbits(bits, axis=1, bitorder="little")
         out = []
-        for row in rows:
-            x = 0
-            for d in reversed(row.tolist()):
-                x = (x << RADIX_BITS) + d
-            out.append(x)
+        for r in range(rows.shape[0]):
+            if canon[r]:
+                x = int.from_bytes(packed[r].tobytes(), "little")
+                out.append(-x if neg[r] else x)
+            else:
+                x = 0
+                for d in reversed(rows[r].tolist()):
+                    x = (x << RADIX_BITS) + d
+                out.append(x)
         return out
 
     def to_digits(self, values) -> np.ndarray:
