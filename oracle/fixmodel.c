@@ -66,7 +66,7 @@ static void tprod_acc(const int32_t *a, const int32_t *b, int L, int T, i128 *co
 
 /* V = sum col[c] B^c (exact), return digits of rnd(V) = floor((V + B^2/2)/B^2) in out[0..Lf];
    returns 1 on overflow (result does not fit Lf+1 digits) */
-static int round_cols(const i128 *col, int ncols, int Lf, int32_t *out) {
+static int round_cols_canon(const i128 *col, int ncols, int Lf, int32_t *out) {
   /* normalize to digits in [0, B) with floor carries, keep the top carry */
   i128 carry = 0;
   int64_t dig[4096 + 8];
@@ -115,6 +115,34 @@ static int round_cols(const i128 *col, int ncols, int Lf, int32_t *out) {
     if (mag[j]) return 1;
   for (int j = 0; j <= Lf; j++) out[j] = neg ? -mag[j] : mag[j];
   return 0;
+}
+
+/* The per-order rounding of the recurrence: digits of rnd(V) in the device's
+   balanced semi-normal form (mpt_device.cuh warp_snf_t). B/2 is added to
+   column 1; three rounds of "every column below the top one (index Lf+2)
+   splits into a balanced digit in [-B/2, B/2) and the carry round(v/B), which
+   moves one column up; the top column absorbs" leave digits in [-B/2-1, B/2];
+   digit 2 is corrected by floor((d_0 + d_1 B) / B^2) and digits 2..Lf+2 are
+   the result. Returns 1 on overflow (|top digit| >= B). */
+static int round_cols(const i128 *col, int ncols, int Lf, int32_t *out) {
+  i128 v[4096 + 8];
+  const int topc = Lf + 2;
+  for (int c = 0; c <= topc; c++) v[c] = c < ncols ? col[c] : 0;
+  for (int c = ncols - 1; c > topc; c--) v[topc] += col[c] << (RADIX_BITS * (c - topc));
+  v[1] += RADIX / 2;
+  for (int r = 0; r < 3; r++) {
+    i128 cin = 0;
+    for (int c = 0; c < topc; c++) {
+      i128 h = (v[c] + RADIX / 2) >> RADIX_BITS;
+      v[c] = v[c] - h * RADIX + cin;
+      cin = h;
+    }
+    v[topc] += cin;
+  }
+  i128 low = v[0] + v[1] * RADIX;
+  v[2] += low < 0 ? -1 : (low >= (i128)RADIX * RADIX ? 1 : 0);
+  for (int j = 0; j <= Lf; j++) out[j] = (int32_t)v[2 + j];
+  return (v[topc] >= RADIX || v[topc] <= -RADIX) ? 1 : 0;
 }
 
 static int build(model_t *M, int D, int NT, const int32_t *teq, const int32_t *tj, const int32_t *tk) {
@@ -249,7 +277,7 @@ static int sum_rows(const model_t *M, const int32_t *coef, int32_t *state, int p
     memset(col, 0, sizeof(i128) * (Wd + 3));
     for (int i = 0; i <= N; i++)
       for (int j = 0; j <= Lf; j++) col[2 + j] += (i128)coef[((size_t)m * (N + 1) + i) * Wd + j];
-    if (round_cols(col, Wd + 3, Lf, state + (size_t)m * Wd)) rc = 1;
+    if (round_cols_canon(col, Wd + 3, Lf, state + (size_t)m * Wd)) rc = 1;
     if (round_prec(state + (size_t)m * Wd, Wd, prec)) rc = 1;
   }
   return rc;

@@ -16,7 +16,8 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
-SOURCES = ("csrc/taylor_kernel.cu", "csrc/taylor_cluster.cu", "csrc/taylor_pipe.cu", "csrc/taylor_grid.cu", "csrc/capi.cu")
+SOURCES = ("csrc/taylor_kernel.cu", "csrc/taylor_cluster.cu", "csrc/taylor_pipe.cu", "csrc/taylor_grid.cu",
+           "csrc/taylor_relay.cu", "csrc/capi.cu")
 OUT = os.path.join(HERE, "_lib", "libmptaylor_b200.so")
 ARCH = ("-gencode", "arch=compute_100a,code=sm_100a")
 
@@ -29,18 +30,31 @@ def nvcc() -> str:
 
 
 def build(verbose: bool = False, extra=()) -> str:
+    """Compile every translation unit in parallel (-c), then link the .so."""
+    from concurrent.futures import ThreadPoolExecutor
+
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    cmd = [
-        nvcc(), "-O3", "-lineinfo", "-std=c++17", *ARCH,
-        "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(REPO, "include"),
-        *(["-Xptxas", "-v"] if verbose else []), *extra,
-        "-o", OUT, *[os.path.join(HERE, s) for s in SOURCES],
-    ]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed:\n{res.stdout}\n{res.stderr}")
+    objdir = os.path.join(HERE, "_lib", "obj")
+    os.makedirs(objdir, exist_ok=True)
+    common = [nvcc(), "-O3", "-lineinfo", "-std=c++17", *ARCH, "-Xcompiler", "-fPIC",
+              "-I", os.path.join(REPO, "include"), *(["-Xptxas", "-v"] if verbose else []), *extra]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
+        res = subprocess.run([*common, "-c", "-o", obj, os.path.join(HERE, src)], capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src}:\n{res.stdout}\n{res.stderr}")
+        return obj, res.stderr
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
     if verbose:
-        sys.stderr.write(res.stderr)
+        for _, err in results:
+            sys.stderr.write(err)
+    res = subprocess.run([nvcc(), *ARCH, "-shared", "-o", OUT, *[o for o, _ in results]], capture_output=True,
+                         text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc link failed:\n{res.stdout}\n{res.stderr}")
     return OUT
 
 

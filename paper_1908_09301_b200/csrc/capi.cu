@@ -22,6 +22,10 @@ size_t pipe_smem_bytes(const Params& p, int G);
 bool pipe_supported(const Params& p);
 cudaError_t launch_pipe_kernel(const Params& p, int G, size_t smem, cudaStream_t stream);
 int pipe_max_cluster(const Params& p, size_t smem, int want);
+size_t relay_smem_bytes(const Params& p, int G);
+bool relay_supported(const Params& p);
+cudaError_t launch_relay_kernel(const Params& p, int G, size_t smem, cudaStream_t stream);
+int relay_max_cluster(const Params& p, size_t smem, int want);
 bool grid_supported(const Params& p);
 size_t grid_smem_bytes(const Params& p, int kc);
 size_t grid_scratch_bytes(const Params& p);
@@ -114,6 +118,26 @@ static int choose_kernel(mpt_plan* pl, int kernel, int want) {
     return MPT_OK;
   }
   const int tries[] = {16, 8, 4, 2, 1};
+  // the relay kernel (lead CTA + bulk CTAs) needs the constants and G >= 2
+  if ((kernel == 0 || kernel == 5) && pl->have_constants && mpt::relay_supported(p) && (kernel == 5 || p.n_traj == 1)) {
+    for (int G : tries) {
+      if (G > want || G < 2) continue;
+      size_t s = mpt::relay_smem_bytes(p, G);
+      if (s > (size_t)pl->optin) continue;
+      if (mpt::relay_max_cluster(p, s, G) < 1) continue;
+      pl->kernel = 5;
+      pl->cluster = G;
+      pl->smem_cluster = s;
+      return MPT_OK;
+    }
+  }
+  if (kernel == 5) {
+    if (!pl->have_constants) {
+      pl->kernel = 0;
+      return MPT_OK;
+    }
+    return fail(MPT_EUNSUP, "the relay kernel does not support this system/precision (shared memory)");
+  }
   // the pipelined kernel needs the constants (integer bilinear coefficients)
   if ((kernel == 0 || kernel == 3) && pl->have_constants && mpt::pipe_supported(p)) {
     for (int G : tries) {
@@ -298,6 +322,7 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
                        : strcmp(ek, "cluster") == 0 ? 2
                        : strcmp(ek, "pipe") == 0    ? 3
                        : strcmp(ek, "grid") == 0    ? 4
+                       : strcmp(ek, "relay") == 0   ? 5
                                                     : 0)
                     : 0;
     int want = ec ? atoi(ec) : (n_traj == 1 ? 16 : 1);
@@ -312,7 +337,7 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
 }
 
 int mpt_plan_configure(mpt_plan* pl, int kernel, int cluster) {
-  if (!pl || kernel < 0 || kernel > 4 || cluster < 1 || cluster > 16) return fail(MPT_EINVAL, "bad configuration");
+  if (!pl || kernel < 0 || kernel > 5 || cluster < 1 || cluster > 16) return fail(MPT_EINVAL, "bad configuration");
   return choose_kernel(pl, kernel, cluster);
 }
 
@@ -446,7 +471,9 @@ static int launch(mpt_plan* pl, int n_steps, int start_step, int stride, cudaStr
     CK(cudaMemsetAsync(pl->d_status, 0, sizeof(int32_t) * p.n_traj, stream));
     p.gscratch = pl->d_gscratch;
     CK(mpt::launch_grid_kernel(p, pl->grid_blocks, pl->grid_kc, pl->smem_grid, stream));
-  } else if (pl->kernel == 3)
+  } else if (pl->kernel == 5)
+    CK(mpt::launch_relay_kernel(p, pl->cluster, pl->smem_cluster, stream));
+  else if (pl->kernel == 3)
     CK(mpt::launch_pipe_kernel(p, pl->cluster, pl->smem_cluster, stream));
   else if (pl->kernel == 2)
     CK(mpt::launch_cluster_kernel(p, pl->cluster, pl->smem_cluster, stream));

@@ -25,9 +25,13 @@ struct Acc {
 // s64 += s32 * s32 as ONE instruction (SASS IMAD.WIDE); writing the product
 // in C++ on int64 operands makes nvcc emit a 64x64 multiply sequence.
 __device__ __forceinline__ int64_t mad_wide(int32_t a, int32_t b, int64_t c) {
+#ifdef MPT_MAD_ASM
   int64_t d;
   asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
   return d;
+#else
+  return c + (int64_t)a * (int64_t)b;
+#endif
 }
 
 __device__ __forceinline__ void acc_zero(Acc& a) {
@@ -255,6 +259,153 @@ __device__ __forceinline__ bool warp_normalize_t(const int64_t* col, int ncols, 
 }
 
 // ---------------------------------------------------------------------------
+// Rounding to balanced semi-normal form (SNF) -- the per-order rounding of the
+// recurrence (U_m, coefficient rows, rounded pair sums):
+//     digits of rnd(V) = floor((V + B^2/2) / B^2)
+// Columns above the top digit position (relative column W+1) are folded into
+// it; then three parallel rounds "every column below the top splits into a
+// balanced digit in [-B/2, B/2) and a carry round(v/B) that moves one column
+// up" leave digits in [-B/2-1, B/2]; the top column absorbs carries and keeps
+// the sign. Digit 2 is corrected by floor((d_0 + d_1 B) / B^2). No carry-
+// lookahead and no sign conversion: the digits are a deterministic function of
+// the exact column value (oracle/fixmodel.c round_cols restates it), they fit
+// int32 with |digit| <= B/2 + 2 (except the top one, |top| < B), and small
+// values of either sign keep their leading zero digits (zero-digit skipping).
+// Canonical digits are only produced for the state (warp_normalize_t, drop 0).
+// Overflow: |top digit| >= B.
+// Lane layout: M consecutive columns per lane, aligned so that the top column
+// topc = W + 1 is the last column of lane 31 (lane l, slot j holds column
+// topc - 32 M + 1 + l M + j; columns below 0 are zero). The loop bounds are
+// compile-time, so the rounds are straight-line code with M independent
+// chains per lane.
+template <int M>
+__device__ __forceinline__ bool warp_snf_t(const int64_t* col, int ncols, int W, int32_t* out, int2* info) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int topc = W + 1;
+  const int c0 = topc - 32 * M + 1 + lane * M;  // column of slot 0
+  int64_t v[M];
+#pragma unroll
+  for (int j = 0; j < M; j++) {
+    const int c = c0 + j;
+    v[j] = (c >= 0 && c < ncols) ? col[c] : 0;
+  }
+  if (lane == 31 && ncols > topc + 1) {
+    // columns above the top one (fold carries of the column groups) belong to
+    // the top digit: v_top += sum_u col[u] B^(u - topc), Horner from the top
+    int64_t acc = 0;
+    bool big = false;
+    for (int u = ncols - 1; u > topc; u--) {
+      acc = acc * kRadix + col[u];
+      big |= (acc > (int64_t(1) << 34)) || (acc < -(int64_t(1) << 34));
+    }
+    v[M - 1] = big ? 4 * kRadix : v[M - 1] + acc * kRadix;
+  }
+  if (c0 <= 1 && c0 + M > 1) {  // rounding: + B^2 / 2
+#pragma unroll
+    for (int j = 0; j < M; j++)
+      if (c0 + j == 1) v[j] += kRadix / 2;
+  }
+  // rounds 1-2 in 64 bits, round 3 (|v| < 2^29) in 32 bits
+#pragma unroll
+  for (int rnd = 0; rnd < 2; rnd++) {
+    int64_t h[M];
+#pragma unroll
+    for (int j = 0; j < M; j++) {
+      const int64_t t = v[j] + kRadix / 2;
+      h[j] = t >> kRadixBits;
+      v[j] = (int64_t)(int32_t)(((uint32_t)t & (uint32_t)kMask) - (uint32_t)(kRadix / 2));
+    }
+    if (lane == 31) {  // the top column absorbs
+      v[M - 1] += h[M - 1] * kRadix;
+      h[M - 1] = 0;
+    }
+    int64_t cin = __shfl_up_sync(full, h[M - 1], 1);
+    if (lane == 0) cin = 0;
+#pragma unroll
+    for (int j = M - 1; j >= 1; j--) v[j] += h[j - 1];
+    v[0] += cin;
+  }
+  int32_t w[M];
+  {
+    int32_t h[M];
+#pragma unroll
+    for (int j = 0; j < M; j++) {
+      const int32_t t = (int32_t)v[j] + (int32_t)(kRadix / 2);
+      h[j] = t >> kRadixBits;
+      w[j] = (t & (int32_t)kMask) - (int32_t)(kRadix / 2);
+    }
+    int64_t top = 0;
+    if (lane == 31) {
+      top = v[M - 1];  // top column keeps its full value
+      h[M - 1] = 0;
+    }
+    int32_t cin = __shfl_up_sync(full, h[M - 1], 1);
+    if (lane == 0) cin = 0;
+#pragma unroll
+    for (int j = M - 1; j >= 1; j--) w[j] += h[j - 1];
+    w[0] += cin;
+    if (lane == 31) {
+      top += (M >= 2 ? h[M - 2 < 0 ? 0 : M - 2] : cin);
+      w[M - 1] = (int32_t)(top >= kRadix ? kRadix : (top <= -kRadix ? -kRadix : top));
+    }
+  }
+  // floor((d_0 + d_1 B) / B^2) corrects digit 2 (columns 0, 1, 2 sit in one or two lanes)
+  const int p0 = 32 * M - 1 - topc;  // linear slot of column 0
+  int32_t s0 = 0, s1 = 0;
+#pragma unroll
+  for (int j = 0; j < M; j++) {
+    if (j == p0 % M) s0 = w[j];
+    if (j == (p0 + 1) % M) s1 = w[j];
+  }
+  const int32_t d0 = __shfl_sync(full, s0, p0 / M);
+  const int32_t d1 = __shfl_sync(full, s1, (p0 + 1) / M);
+  const int64_t low = (int64_t)d0 + (int64_t)d1 * kRadix;
+  const int32_t fix = low < 0 ? -1 : (low >= kRadix * kRadix ? 1 : 0);
+  bool ovf = false;
+  int bot = 1 << 30, tp = -1;
+#pragma unroll
+  for (int j = 0; j < M; j++) {
+    const int c = c0 + j;
+    if (c >= 2) {
+      const int d = c - 2;
+      const int32_t dig = w[j] + (c == 2 ? fix : 0);
+      out[d] = dig;
+      if (dig) {
+        bot = min(bot, d);
+        tp = max(tp, d);
+      }
+    }
+  }
+  if (lane == 31 && (w[M - 1] >= kRadix || w[M - 1] <= -kRadix)) ovf = true;
+  bot = __reduce_min_sync(full, bot);
+  tp = __reduce_max_sync(full, tp);
+  if (lane == 0) *info = make_int2(tp >= 0 ? bot : W, tp);
+  const bool any = __any_sync(full, ovf);
+  __syncwarp();
+  return any;
+}
+
+__device__ __forceinline__ bool warp_snf(const int64_t* col, int ncols, int W, int32_t* out, int2* info) {
+  const int M = (W + 2 + 31) / 32;
+  switch (M) {
+    case 1: return warp_snf_t<1>(col, ncols, W, out, info);
+    case 2: return warp_snf_t<2>(col, ncols, W, out, info);
+    case 3: return warp_snf_t<3>(col, ncols, W, out, info);
+    case 4: return warp_snf_t<4>(col, ncols, W, out, info);
+    case 5: return warp_snf_t<5>(col, ncols, W, out, info);
+    case 6: return warp_snf_t<6>(col, ncols, W, out, info);
+    case 7: return warp_snf_t<7>(col, ncols, W, out, info);
+    case 8: return warp_snf_t<8>(col, ncols, W, out, info);
+    case 9: return warp_snf_t<9>(col, ncols, W, out, info);
+    case 10: return warp_snf_t<10>(col, ncols, W, out, info);
+    case 11: case 12: return warp_snf_t<12>(col, ncols, W, out, info);
+    case 13: case 14: case 15: case 16: return warp_snf_t<16>(col, ncols, W, out, info);
+    default: return warp_snf_t<kMaxLanesDigits>(col, ncols, W, out, info);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Group normalisation: NW warps (named barrier `bar_id`, 32*NW threads) share
 // one column vector; warp w of the group owns columns [w*32*m, (w+1)*32*m).
 // Same algorithm as warp_normalize_t (three parallel carry rounds, then a
@@ -465,6 +616,7 @@ __device__ __forceinline__ bool warp_normalize_upto(const int64_t* col, int ncol
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int m = (ncols + 31) / 32;
+  if (drop == 2 && round_prec_bits == 0) return warp_snf(col, ncols, W, out, info);
   bool ovf;
   if (m <= 2)
     ovf = warp_normalize_t<2>(col, ncols, drop, W, out);
@@ -501,6 +653,14 @@ static __device__ __noinline__ bool group_normalize(const int64_t* col, int ncol
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int m = (ncols + 32 * NW - 1) / (32 * NW);
+  if (drop == 2 && round_prec_bits == 0) {  // SNF: one warp of the group, the others wait
+    if (gw == 0 && warp_snf(col, ncols, W, out, info) && lane == 0) xs[0] = 1;
+    else if (gw == 0 && lane == 0) xs[0] = 0;
+    group_sync(bar_id, 32 * NW);
+    const bool o = xs[0] != 0;
+    group_sync(bar_id, 32 * NW);
+    return o;
+  }
   bool ovf;
   if (m <= 2)
     ovf = group_normalize_t<2>(col, ncols, drop, W, out, gw, NW, bar_id, xs);
@@ -541,6 +701,39 @@ static __device__ __noinline__ bool group_normalize(const int64_t* col, int ncol
   }
   group_sync(bar_id, 32 * NW);
   return ovf;
+}
+
+// ---------------------------------------------------------------------------
+// Folded partial units: a thread's (column group, operand slice) accumulator
+// is stored as kR uint32 digits (relative columns c0-T .. c0-T+kR-1) plus the
+// group's outgoing carry; a column's total over n units u0, u0+ustride, ... is
+// the digits of the group owning it plus the carry of the group below.
+__device__ __forceinline__ void unit_store(uint32_t* part, int64_t* pcar, const Acc& a, int grp, int c0, int T) {
+#pragma unroll
+  for (int r = 0; r < kR; r++) {
+    const int c = c0 + r - T;
+    if (c >= 0) part[c] = (uint32_t)a.v[r];
+  }
+  pcar[grp] = a.v[kR];
+}
+
+__device__ __forceinline__ int64_t unit_column(const uint32_t* part, const int64_t* pcar, int u0, int ustride, int n,
+                                               int ncx, int ngstride, int c, int T, int gf, int ng) {
+  const int cabs = c + T;
+  const int own = cabs / kR - gf;
+  const int cgb = (cabs % kR == 0) ? cabs / kR - 1 - gf : -1;
+  int64_t s = 0;
+  if (own >= 0 && own < ng) {
+    const uint32_t* pp = part + (size_t)u0 * ncx + c;
+#pragma unroll 4
+    for (int u = 0; u < n; u++) s += pp[(size_t)u * ustride * ncx];
+  }
+  if (cgb >= 0 && cgb < ng) {
+    const int64_t* pc = pcar + (size_t)u0 * ngstride + cgb;
+#pragma unroll 4
+    for (int u = 0; u < n; u++) s += pc[(size_t)u * ustride * ngstride];
+  }
+  return s;
 }
 
 }  // namespace mpt

@@ -107,10 +107,10 @@ class DevicePlan:
         kern, cl = ctypes.c_int32(), ctypes.c_int32()
         _native.check(self.lib.mpt_plan_kernel(self.h, ctypes.byref(kern), ctypes.byref(cl)))
         return {"smem_bytes": s.value, "k_chunk": k.value, "threads": t.value,
-                "kernel": {1: "team", 2: "cluster", 3: "pipe", 4: "grid"}.get(kern.value, "?"), "cluster": cl.value}
+                "kernel": {1: "team", 2: "cluster", 3: "pipe", 4: "grid", 5: "relay"}.get(kern.value, "?"), "cluster": cl.value}
 
     def configure(self, kernel: str = "auto", cluster: int = 8):
-        code = {"auto": 0, "team": 1, "cluster": 2, "pipe": 3, "grid": 4}[kernel]
+        code = {"auto": 0, "team": 1, "cluster": 2, "pipe": 3, "grid": 4, "relay": 5}[kernel]
         _native.check(self.lib.mpt_plan_configure(self.h, code, cluster))
 
     def _state(self, state: np.ndarray) -> np.ndarray:

@@ -51,6 +51,7 @@ def test_integrate_bit_exact_vs_model(gpu, P, N, steps, stride):
 
 @pytest.mark.parametrize("kernel,cluster", [("team", 1), ("cluster", 1), ("cluster", 2), ("cluster", 8),
                                             ("cluster", 16), ("pipe", 1), ("pipe", 2), ("pipe", 4), ("pipe", 16),
+                                            ("relay", 2), ("relay", 3), ("relay", 8), ("relay", 16),
                                             ("grid", 1)])
 @pytest.mark.parametrize("P,N,steps", [(167, 40, 12), (1661, 200, 2)])
 def test_every_kernel_bit_exact_vs_model(gpu, kernel, cluster, P, N, steps):

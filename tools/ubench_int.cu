@@ -45,6 +45,7 @@ __global__ void kern(int iters, const int32_t* __restrict__ in, long long* out) 
         if (V == 1) a64[c] = (int64_t)mad_wide_u((uint32_t)x[c], (uint32_t)yy, (uint64_t)a64[c]);
         if (V == 2) asm volatile("mad.lo.u32 %0, %1, %2, %0;" : "+r"(a32[c]) : "r"(x[c]), "r"(yy));  // IMAD
         if (V == 3) ad[c] = fma((double)x[c], (double)yy, ad[c]);      // DFMA (conversion hoisted?)
+        if (V == 4) a64[c] += (int64_t)x[c] * (int64_t)yy;             // C++ form: fused IMAD.WIDE
       }
     }
     y += i;
@@ -82,11 +83,11 @@ int main() {
   for (int i = 0; i < 1024; i++) h[i] = (i * 2654435761u) >> 4;
   cudaMemcpy(d_in, h, sizeof h, cudaMemcpyHostToDevice);
   const char* names[] = {"mad.wide.s32 (s64 += s32*s32)", "mad.wide.u32 (u64 += u32*u32)",
-                         "mad.lo.u32 (u32 += u32*u32)", "fma.rn.f64"};
-  double r[4] = {run<0>(sms, d_in, d_out), run<1>(sms, d_in, d_out), run<2>(sms, d_in, d_out),
-                 run<3>(sms, d_in, d_out)};
+                         "mad.lo.u32 (u32 += u32*u32)", "fma.rn.f64", "C++ s64 += (s64)s32*(s64)s32"};
+  double r[5] = {run<0>(sms, d_in, d_out), run<1>(sms, d_in, d_out), run<2>(sms, d_in, d_out),
+                 run<3>(sms, d_in, d_out), run<4>(sms, d_in, d_out)};
   printf("{\"sms\": %d, \"clock_khz\": %d, \"results\": [", sms, clk);
-  for (int v = 0; v < 4; v++)
+  for (int v = 0; v < 5; v++)
     printf("%s{\"op\": \"%s\", \"per_second\": %.4e, \"per_clk_per_sm\": %.2f}", v ? ", " : "", names[v], r[v],
            r[v] / (sms * (double)clk * 1e3));
   printf("]}\n");
