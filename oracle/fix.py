@@ -42,13 +42,24 @@ def _tables(t):
     return nt, keep
 
 
-def compute_jet(tables, frac_digits: int, order: int, state: np.ndarray) -> np.ndarray:
-    """-> coef[dim, order+1, W] (digits), exactly as the kernel computes them."""
+def _bulk(bulk):
+    if bulk is not None:
+        lib().fix_set_bulk(int(bulk))
+
+
+def compute_jet(tables, frac_digits: int, order: int, state: np.ndarray, variant: int = 0,
+                bulk: int | None = None) -> np.ndarray:
+    """-> coef[dim, order+1, W] (digits), exactly as the kernel computes them.
+
+    variant 0: per-order C-product recurrence (team/cluster/pipe/relay/grid
+    kernels); variant 1: matrix recurrence (mx kernel) with `bulk` bulk CTAs
+    (the partition of the Cauchy sums enters its rounding)."""
+    _bulk(bulk)
     W = frac_digits + 1
     nt, k = _tables(tables)
     st = np.ascontiguousarray(state, dtype=np.int32).reshape(tables.dim, W)
     out = np.zeros((tables.dim, order + 1, W), np.int32)
-    rc = lib().fix_compute_jet(tables.dim, nt, _p(k[0]), _p(k[1]), _p(k[2]), frac_digits,
+    rc = lib().fix_compute_jet_v(variant, tables.dim, nt, _p(k[0]), _p(k[1]), _p(k[2]), frac_digits,
                                tables.c_shift, order, _p(k[3]), _p(k[4]), _p(k[5]), _p(k[6]),
                                _p(st), out.ctypes.data_as(_i32p))
     if rc:
@@ -57,15 +68,16 @@ def compute_jet(tables, frac_digits: int, order: int, state: np.ndarray) -> np.n
 
 
 def integrate(tables, frac_digits: int, order: int, prec_bits: int, state0: np.ndarray,
-              n_steps: int, start_step: int = 0, stride: int = 1):
+              n_steps: int, start_step: int = 0, stride: int = 1, variant: int = 0, bulk: int | None = None):
     """-> (steps, records[nrec, dim, W]) on the reference's record grid."""
+    _bulk(bulk)
     W = frac_digits + 1
     nt, k = _tables(tables)
     st = np.ascontiguousarray(state0, dtype=np.int32).reshape(tables.dim, W)
     max_rec = (n_steps - start_step) // stride + 3
     steps = np.zeros(max_rec, np.int32)
     recs = np.zeros((max_rec, tables.dim, W), np.int32)
-    nrec = lib().fix_integrate(tables.dim, nt, _p(k[0]), _p(k[1]), _p(k[2]), frac_digits,
+    nrec = lib().fix_integrate_v(variant, tables.dim, nt, _p(k[0]), _p(k[1]), _p(k[2]), frac_digits,
                                tables.c_shift, order, prec_bits, _p(k[3]), _p(k[4]), _p(k[5]),
                                _p(k[6]), _p(st), n_steps, start_step, stride, max_rec,
                                steps.ctypes.data_as(_i32p), recs.ctypes.data_as(_i32p))

@@ -41,6 +41,7 @@ typedef __int128 i128;
 
 typedef struct {
   int D, NT, NP, Lf, sc, order;
+  int variant; /* 0: per-order C-product recurrence, 1: matrix recurrence (jet_mx) */
   const int32_t *cst;  /* D x W */
   const int32_t *lin;  /* D x D x W */
   const int32_t *q;    /* NT x W */
@@ -57,6 +58,20 @@ static void tprod_acc(const int32_t *a, const int32_t *b, int L, int T, i128 *co
     int q0 = T - p;
     if (q0 < 0) q0 = 0;
     for (int q = q0; q < L; q++) {
+      int c = p + q - T;
+      if (c >= ncols) break;
+      col[c] += (i128)((int64_t)a[p] * (int64_t)b[q]);
+    }
+  }
+}
+
+/* tprod_acc for operands of different lengths */
+static void tprod_acc2(const int32_t *a, int La, const int32_t *b, int Lb, int T, i128 *col, int ncols) {
+  for (int p = 0; p < La; p++) {
+    if (!a[p]) continue;
+    int q0 = T - p;
+    if (q0 < 0) q0 = 0;
+    for (int q = q0; q < Lb; q++) {
       int c = p + q - T;
       if (c >= ncols) break;
       col[c] += (i128)((int64_t)a[p] * (int64_t)b[q]);
@@ -145,6 +160,53 @@ static int round_cols(const i128 *col, int ncols, int Lf, int32_t *out) {
   return (v[topc] >= RADIX || v[topc] <= -RADIX) ? 1 : 0;
 }
 
+/* Rounding of the matrix recurrence (variant 1): digits of
+ *     R = floor((V + B^2/2) / B^2),   V = sum_c col[c] B^c   (exact)
+ * in the UNIQUE balanced form: R = sum_{j<Wout-1} e_j B^j + e_top B^(Wout-1)
+ * with every e_j (top included) in [-B/2, B/2). Unlike round_cols the result
+ * depends on the value V only, not on how it is split over the columns, so a
+ * device that folds partial column sums differently still agrees bit for bit.
+ * Small values of either sign keep leading zero digits. Returns 1 on overflow. */
+static int round_bnf(const i128 *col, int ncols, int Wout, int32_t *out) {
+  int64_t dig[4096 + 16];
+  i128 carry = 0;
+  for (int c = 0; c < ncols; c++) {
+    i128 v = col[c] + carry + (c == 1 ? (RADIX / 2) : 0);
+    i128 d = v & (RADIX - 1);
+    carry = (v - d) >> RADIX_BITS;
+    dig[c] = (int64_t)d;
+  }
+  for (int c = ncols; c < Wout + 2; c++) {
+    i128 v = carry;
+    i128 d = v & (RADIX - 1);
+    carry = (v - d) >> RADIX_BITS;
+    dig[c] = (int64_t)d;
+  }
+  const int n = ncols > Wout + 2 ? ncols : Wout + 2;
+  /* everything above the top digit column (Wout+1) must vanish in two's complement */
+  int ovf = 0;
+  i128 hi = carry;
+  for (int c = n - 1; c > Wout + 1; c--) {
+    hi = hi * RADIX + dig[c];
+    if (hi > ((i128)1 << 40) || hi < -((i128)1 << 40)) ovf = 1;
+  }
+  int t = 0;
+  for (int j = 0; j < Wout - 1; j++) {
+    int64_t x = dig[2 + j] + t;
+    if (x >= RADIX / 2) {
+      x -= RADIX;
+      t = 1;
+    } else {
+      t = 0;
+    }
+    out[j] = (int32_t)x;
+  }
+  i128 top = (i128)dig[Wout + 1] + t + hi * RADIX;
+  if (top >= RADIX / 2 || top < -(RADIX / 2)) ovf = 1;
+  out[Wout - 1] = (int32_t)top;
+  return ovf;
+}
+
 static int build(model_t *M, int D, int NT, const int32_t *teq, const int32_t *tj, const int32_t *tk) {
   if (D > 16 || NT > 64) return -3;
   M->D = D;
@@ -230,6 +292,159 @@ static int jet(const model_t *M, int32_t *coef) {
   return rc;
 }
 
+/* ---------------------------------------------------------------------------
+ * Matrix recurrence (variant 1; paper_1908_09301_b200/csrc/taylor_mx.cu).
+ * Same quantities, reassociated so that one order costs one product stage and
+ * one rounding on the critical path. With a~_{i+1} = C_i U_i the next
+ * numerator is linear in U_i except for the Cauchy sums; the Cauchy sum of
+ * order j = i+1 is split into its lag-1 terms (rows j-1 and 1, computed next
+ * to the recurrence) and the rest L'(j) (rows 2..j-2, computed ahead by the
+ * bulk CTAs, owner(k) = 1 + (k-1) mod Gb):
+ *
+ *   U_j^m = rnd( sum_{j'} tprod(U_i^{j'}, K_i^{m,j'}, Lf+sc-2)
+ *               + sum_{t in m} q_t [ lag_t(j) + sum_o split1(P_{o,t}(j)) ] )
+ *   K_i^{m,j'} = rnd_{Lf+2 digits}( tprod(S^{m,j'}, C_i, Lf-2) )  (keeps the sc digits of C_i)
+ *   S^{m,j'} = bnf( lin[m][j'] + sum_{t in m, j_t=j'} q_t a~^{k_t}_0 + sum_{t in m, k_t=j'} q_t a~^{j_t}_0 )
+ *   lag_t(2) = tprod(a~^a_1, a~^b_1),  lag_t(j>=3) = tprod(a~^a_{j-1}, a~^b_1) + tprod(a~^a_1, a~^b_{j-1})
+ *   P_{o,t}(j) = sum_{k in [2, j-2], owner(k) = o} tprod(a~^a_{j-k}, a~^b_k, Lf-2)       (exact)
+ *   split1(P)[c] = (P_c mod B) + floor(P_{c-1} / B)   (one carry step, a function of P only)
+ *   a~^m_{i+1} = rnd( tprod(U_i^m, C_i, Lf+sc-2) )
+ *   U_0 = rnd( cst B^2 + sum_j tprod(lin[m][j], bnf(a~_0^j)) + sum_t q_t tprod(bnf(a~_0^a), bnf(a~_0^b)) )
+ *
+ * rnd = round_cols applied to EXACT column sums (the device forms them in
+ * int64 without folds: every operand digit is balanced or semi-normal), so
+ * the rounding is deterministic; bnf = value-exact balanced digits (drop 0).
+ * Requires small-integer bilinear coefficients.
+ */
+static int bnf_exact(const i128 *val, int n, int Wout, int32_t *out) {
+  /* balanced digits of V = sum val[c] B^c (no rounding): round_bnf with the two
+     guard columns zero and the rounding half cancelled */
+  i128 col[4096 + 8];
+  col[0] = -(RADIX / 2);
+  col[1] = 0;
+  for (int c = 0; c < n; c++) col[2 + c] = val[c];
+  return round_bnf(col, n + 2, Wout, out);
+}
+
+static void split1(const i128 *P, int ncols, i128 *acc, int64_t mult) {
+  i128 prev = 0;
+  for (int c = 0; c < ncols; c++) {
+    i128 lo = P[c] & (RADIX - 1);
+    i128 hi_prev = prev >> RADIX_BITS; /* floor */
+    acc[c] += (i128)mult * (lo + hi_prev);
+    prev = P[c];
+  }
+}
+
+static int mx_bulk = 15;
+void fix_set_bulk(int Gb) { mx_bulk = Gb < 1 ? 1 : Gb; }
+
+static int jet_mx(const model_t *M, int32_t *coef) {
+  int Lf = M->Lf, L = Lf + 1, Wd = W(M), D = M->D, N = M->order, sc = M->sc, Gb = mx_bulk;
+  int ncols = Lf + 4, KW = Wd + 1;
+  int64_t qint[64];
+  for (int t = 0; t < M->NT; t++)
+    if (!small_int(M->q + (size_t)t * Wd, Lf, &qint[t])) return -5;
+  i128 *col = malloc(sizeof(i128) * (size_t)(ncols + 2));
+  i128 *P = malloc(sizeof(i128) * (size_t)(ncols + 2));
+  int32_t *SB = malloc(sizeof(int32_t) * (size_t)D * Wd);
+  int32_t *S = calloc((size_t)D * D * Wd, sizeof(int32_t));
+  int32_t *K = malloc(sizeof(int32_t) * (size_t)D * D * KW);
+  int32_t *U = malloc(sizeof(int32_t) * (size_t)D * Wd);
+  int32_t *U2 = malloc(sizeof(int32_t) * (size_t)D * Wd);
+  int snz[256];
+  i128 acc[4096 + 8];
+  int rc = 0;
+#define CO(m, i) (coef + ((size_t)(m) * (N + 1) + (i)) * Wd)
+  for (int m = 0; m < D && !rc; m++) {
+    for (int d = 0; d <= Lf; d++) acc[d] = CO(m, 0)[d];
+    if (bnf_exact(acc, Wd, Wd, SB + (size_t)m * Wd)) rc = 1;
+  }
+  for (int m = 0; m < D && !rc; m++)
+    for (int j = 0; j < D && !rc; j++) {
+      for (int d = 0; d <= Lf; d++) acc[d] = M->lin[((size_t)m * D + j) * Wd + d];
+      for (int t = 0; t < M->NT; t++) {
+        if (M->teq[t] != m) continue;
+        if (M->tj[t] == j)
+          for (int d = 0; d <= Lf; d++) acc[d] += (i128)qint[t] * CO(M->tk[t], 0)[d];
+        if (M->tk[t] == j)
+          for (int d = 0; d <= Lf; d++) acc[d] += (i128)qint[t] * CO(M->tj[t], 0)[d];
+      }
+      int32_t *s = S + ((size_t)m * D + j) * Wd;
+      if (bnf_exact(acc, Wd, Wd, s)) rc = 1;
+      snz[m * D + j] = 0;
+      for (int d = 0; d <= Lf; d++) snz[m * D + j] |= s[d] != 0;
+    }
+  for (int m = 0; m < D && !rc; m++) {
+    memset(col, 0, sizeof(i128) * ncols);
+    for (int j = 0; j <= Lf; j++) col[2 + j] += (i128)M->cst[(size_t)m * Wd + j];
+    for (int j = 0; j < D; j++) tprod_acc(M->lin + ((size_t)m * D + j) * Wd, SB + (size_t)j * Wd, L, Lf - 2, col, ncols);
+    for (int t = 0; t < M->NT; t++) {
+      if (M->teq[t] != m) continue;
+      memset(P, 0, sizeof(i128) * ncols);
+      tprod_acc(SB + (size_t)M->tj[t] * Wd, SB + (size_t)M->tk[t] * Wd, L, Lf - 2, P, ncols);
+      for (int c = 0; c < ncols; c++) col[c] += (i128)qint[t] * P[c];
+    }
+    if (round_cols(col, ncols, Lf, U + (size_t)m * Wd)) rc = 1;
+  }
+  for (int i = 0; i < N && !rc; i++) {
+    const int32_t *C = M->ctab + (size_t)i * Wd;
+    for (int m = 0; m < D; m++) {
+      memset(col, 0, sizeof(i128) * ncols);
+      tprod_acc(U + (size_t)m * Wd, C, L, Lf + sc - 2, col, ncols);
+      if (round_cols(col, ncols, Lf, CO(m, i + 1))) rc = 1;
+    }
+    if (i + 1 >= N) break;
+    for (int e = 0; e < D * D; e++) {
+      if (!snz[e]) continue;
+      memset(col, 0, sizeof(i128) * ncols);
+      tprod_acc(S + (size_t)e * Wd, C, L, Lf - 2, col, ncols);
+      if (round_cols(col, ncols, Lf + 1, K + (size_t)e * KW)) rc = 1;
+    }
+    const int j = i + 1;
+    for (int m = 0; m < D; m++) {
+      memset(col, 0, sizeof(i128) * ncols);
+      for (int jj = 0; jj < D; jj++)
+        if (snz[m * D + jj])
+          tprod_acc2(U + (size_t)jj * Wd, L, K + ((size_t)m * D + jj) * KW, KW, Lf + sc - 2, col, ncols);
+      for (int t = 0; t < M->NT; t++) {
+        if (M->teq[t] != m) continue;
+        const int a = M->tj[t], b = M->tk[t];
+        memset(P, 0, sizeof(i128) * ncols);
+        if (j == 2) tprod_acc(CO(a, 1), CO(b, 1), L, Lf - 2, P, ncols);
+        if (j >= 3) {
+          tprod_acc(CO(a, j - 1), CO(b, 1), L, Lf - 2, P, ncols);
+          tprod_acc(CO(a, 1), CO(b, j - 1), L, Lf - 2, P, ncols);
+        }
+        for (int c = 0; c < ncols; c++) col[c] += (i128)qint[t] * P[c];
+        for (int o = 1; o <= Gb; o++) {
+          memset(P, 0, sizeof(i128) * ncols);
+          int any = 0;
+          for (int k = 2; k <= j - 2; k++) {
+            if (1 + (k - 1) % Gb != o) continue;
+            tprod_acc(CO(a, j - k), CO(b, k), L, Lf - 2, P, ncols);
+            any = 1;
+          }
+          if (any) split1(P, ncols, col, qint[t]);
+        }
+      }
+      if (round_cols(col, ncols, Lf, U2 + (size_t)m * Wd)) rc = 1;
+    }
+    memcpy(U, U2, sizeof(int32_t) * (size_t)D * Wd);
+  }
+#undef CO
+  free(col);
+  free(P);
+  free(SB);
+  free(S);
+  free(K);
+  free(U);
+  free(U2);
+  return rc;
+}
+
+static int jet_any(const model_t *M, int32_t *coef) { return M->variant == 1 ? jet_mx(M, coef) : jet(M, coef); }
+
 /* round the canonical digit vector to `prec` significant bits, ties to even */
 static int round_prec(int32_t *d, int W, int prec) {
   int tp = -1;
@@ -283,7 +498,7 @@ static int sum_rows(const model_t *M, const int32_t *coef, int32_t *state, int p
   return rc;
 }
 
-int fix_compute_jet(int D, int NT, const int32_t *teq, const int32_t *tj, const int32_t *tk, int Lf,
+int fix_compute_jet_v(int variant, int D, int NT, const int32_t *teq, const int32_t *tj, const int32_t *tk, int Lf,
                     int sc, int order, const int32_t *cst, const int32_t *lin, const int32_t *q,
                     const int32_t *ctab, const int32_t *state, int32_t *coef_out) {
   model_t M;
@@ -297,14 +512,15 @@ int fix_compute_jet(int D, int NT, const int32_t *teq, const int32_t *tj, const 
   M.lin = lin;
   M.q = q;
   M.ctab = ctab;
+  M.variant = variant;
   int Wd = Lf + 1;
   for (int m = 0; m < D; m++)
     memcpy(coef_out + (size_t)m * (order + 1) * Wd, state + (size_t)m * Wd, sizeof(int32_t) * Wd);
-  return jet(&M, coef_out);
+  return jet_any(&M, coef_out);
 }
 
 /* records: step start, every multiple of stride, and n_steps; returns #records or <0 */
-int fix_integrate(int D, int NT, const int32_t *teq, const int32_t *tj, const int32_t *tk, int Lf,
+int fix_integrate_v(int variant, int D, int NT, const int32_t *teq, const int32_t *tj, const int32_t *tk, int Lf,
                   int sc, int order, int prec, const int32_t *cst, const int32_t *lin, const int32_t *q,
                   const int32_t *ctab, const int32_t *state0, int n_steps, int start_step,
                   int stride, int max_rec, int32_t *rec_step, int32_t *rec_state) {
@@ -319,6 +535,7 @@ int fix_integrate(int D, int NT, const int32_t *teq, const int32_t *tj, const in
   M.lin = lin;
   M.q = q;
   M.ctab = ctab;
+  M.variant = variant;
   int Wd = Lf + 1;
   int32_t *coef = malloc(sizeof(int32_t) * (size_t)D * (order + 1) * Wd);
   int32_t *state = malloc(sizeof(int32_t) * (size_t)D * Wd);
@@ -332,7 +549,7 @@ int fix_integrate(int D, int NT, const int32_t *teq, const int32_t *tj, const in
   for (int n = start_step + 1; n <= n_steps; n++) {
     for (int m = 0; m < D; m++)
       memcpy(coef + (size_t)m * (order + 1) * Wd, state + (size_t)m * Wd, sizeof(int32_t) * Wd);
-    if (jet(&M, coef) || sum_rows(&M, coef, state, prec)) { rc = -1; goto out; }
+    if (jet_any(&M, coef) || sum_rows(&M, coef, state, prec)) { rc = -1; goto out; }
     if (n % stride == 0 || n == n_steps) {
       if (nrec >= max_rec) { rc = -2; goto out; }
       rec_step[nrec] = n;
@@ -344,4 +561,18 @@ out:
   free(coef);
   free(state);
   return rc < 0 ? rc : nrec;
+}
+
+int fix_compute_jet(int D, int NT, const int32_t *teq, const int32_t *tj, const int32_t *tk, int Lf, int sc,
+                    int order, const int32_t *cst, const int32_t *lin, const int32_t *q, const int32_t *ctab,
+                    const int32_t *state, int32_t *coef_out) {
+  return fix_compute_jet_v(0, D, NT, teq, tj, tk, Lf, sc, order, cst, lin, q, ctab, state, coef_out);
+}
+
+int fix_integrate(int D, int NT, const int32_t *teq, const int32_t *tj, const int32_t *tk, int Lf, int sc,
+                  int order, int prec, const int32_t *cst, const int32_t *lin, const int32_t *q,
+                  const int32_t *ctab, const int32_t *state0, int n_steps, int start_step, int stride,
+                  int max_rec, int32_t *rec_step, int32_t *rec_state) {
+  return fix_integrate_v(0, D, NT, teq, tj, tk, Lf, sc, order, prec, cst, lin, q, ctab, state0, n_steps,
+                         start_step, stride, max_rec, rec_step, rec_state);
 }

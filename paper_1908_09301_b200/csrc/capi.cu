@@ -31,6 +31,11 @@ size_t grid_smem_bytes(const Params& p, int kc);
 size_t grid_scratch_bytes(const Params& p);
 cudaError_t launch_grid_kernel(const Params& p, int nblocks, int kc, size_t smem, cudaStream_t stream);
 int grid_max_blocks(const Params& p, size_t smem);
+size_t mx_smem_bytes(const Params& p, int G);
+size_t mx_scratch_bytes(const Params& p);
+bool mx_supported(const Params& p);
+cudaError_t launch_mx_kernel(const Params& p, int G, size_t smem, cudaStream_t stream);
+int mx_max_cluster(const Params& p, size_t smem, int want);
 }  // namespace mpt
 
 static thread_local std::string g_err;
@@ -62,7 +67,8 @@ struct mpt_plan {
   bool have_constants = false;
   unsigned long long* d_counters = nullptr;
   bool counting = false;
-  int kernel = 0;    // 1 team (rows in HBM/L2), 2 cluster (rows in smem), 3 pipeline, 4 grid (all SMs)
+  int kernel = 0;    // 1 team (rows in HBM/L2), 2 cluster (rows in smem), 3 pipeline, 4 grid (all SMs),
+                     // 5 relay, 6 mx (matrix recurrence)
   int cluster = 1;   // CTAs per trajectory for the cluster kernel
   size_t smem_cluster = 0;
   int optin = 0;
@@ -70,6 +76,8 @@ struct mpt_plan {
   int grid_blocks = 0, grid_kc = 0;
   size_t smem_grid = 0;
   void* d_gscratch = nullptr;
+  void* d_mxscratch = nullptr;
+  size_t mxscratch_bytes = 0;
 };
 
 static int setup_grid(mpt_plan* pl) {
@@ -118,6 +126,34 @@ static int choose_kernel(mpt_plan* pl, int kernel, int want) {
     return MPT_OK;
   }
   const int tries[] = {16, 8, 4, 2, 1};
+  // the matrix-recurrence kernel (lead CTA + bulk CTAs, K table in global memory)
+  if ((kernel == 0 || kernel == 6) && pl->have_constants && mpt::mx_supported(p) && (kernel == 6 || p.n_traj == 1)) {
+    for (int G : tries) {
+      if (G > want || G < 2) continue;
+      size_t s = mpt::mx_smem_bytes(p, G);
+      if (s > (size_t)pl->optin) continue;
+      if (mpt::mx_max_cluster(p, s, G) < 1) continue;
+      const size_t need = mpt::mx_scratch_bytes(p);
+      if (need > pl->mxscratch_bytes) {
+        cudaFree(pl->d_mxscratch);
+        pl->d_mxscratch = nullptr;
+        pl->mxscratch_bytes = 0;
+        CK(cudaMalloc(&pl->d_mxscratch, need));
+        pl->mxscratch_bytes = need;
+      }
+      pl->kernel = 6;
+      pl->cluster = G;
+      pl->smem_cluster = s;
+      return MPT_OK;
+    }
+  }
+  if (kernel == 6) {
+    if (!pl->have_constants) {
+      pl->kernel = 0;
+      return MPT_OK;
+    }
+    return fail(MPT_EUNSUP, "the mx kernel does not support this system/precision");
+  }
   // the relay kernel (lead CTA + bulk CTAs) needs the constants and G >= 2
   if ((kernel == 0 || kernel == 5) && pl->have_constants && mpt::relay_supported(p) && (kernel == 5 || p.n_traj == 1)) {
     for (int G : tries) {
@@ -323,6 +359,7 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
                        : strcmp(ek, "pipe") == 0    ? 3
                        : strcmp(ek, "grid") == 0    ? 4
                        : strcmp(ek, "relay") == 0   ? 5
+                       : strcmp(ek, "mx") == 0      ? 6
                                                     : 0)
                     : 0;
     int want = ec ? atoi(ec) : (n_traj == 1 ? 16 : 1);
@@ -337,7 +374,7 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
 }
 
 int mpt_plan_configure(mpt_plan* pl, int kernel, int cluster) {
-  if (!pl || kernel < 0 || kernel > 5 || cluster < 1 || cluster > 16) return fail(MPT_EINVAL, "bad configuration");
+  if (!pl || kernel < 0 || kernel > 6 || cluster < 1 || cluster > 16) return fail(MPT_EINVAL, "bad configuration");
   return choose_kernel(pl, kernel, cluster);
 }
 
@@ -361,6 +398,7 @@ int mpt_plan_destroy(mpt_plan* pl) {
   cudaFree(pl->d_status);
   cudaFree(pl->d_counters);
   cudaFree(pl->d_gscratch);
+  cudaFree(pl->d_mxscratch);
   if (pl->ev0) cudaEventDestroy(pl->ev0);
   if (pl->ev1) cudaEventDestroy(pl->ev1);
   delete pl;
@@ -454,8 +492,8 @@ static int launch(mpt_plan* pl, int n_steps, int start_step, int stride, cudaStr
   mpt::Params p = pl->p;
   p.write_coef = write_coef;
   if (getenv("MPT_DEBUG")) {
-    if (!g_dbg) cudaMalloc((void**)&g_dbg, 8 * 4096);
-    cudaMemset(g_dbg, 0, 8 * 4096);
+    if (!g_dbg) cudaMalloc((void**)&g_dbg, 8 * 65536);
+    cudaMemset(g_dbg, 0, 8 * 65536);
     p.dbg = g_dbg;
   } else {
     p.dbg = nullptr;
@@ -471,6 +509,10 @@ static int launch(mpt_plan* pl, int n_steps, int start_step, int stride, cudaStr
     CK(cudaMemsetAsync(pl->d_status, 0, sizeof(int32_t) * p.n_traj, stream));
     p.gscratch = pl->d_gscratch;
     CK(mpt::launch_grid_kernel(p, pl->grid_blocks, pl->grid_kc, pl->smem_grid, stream));
+  } else if (pl->kernel == 6) {
+    CK(cudaMemsetAsync(pl->d_status, 0, sizeof(int32_t) * p.n_traj, stream));
+    p.gscratch = pl->d_mxscratch;
+    CK(mpt::launch_mx_kernel(p, pl->cluster, pl->smem_cluster, stream));
   } else if (pl->kernel == 5)
     CK(mpt::launch_relay_kernel(p, pl->cluster, pl->smem_cluster, stream));
   else if (pl->kernel == 3)

@@ -1,0 +1,1107 @@
+// Matrix-recurrence kernel ("mx"): one trajectory per thread-block cluster of
+// G = 2..16 CTAs (sm_100a); the per-order critical path runs on CTA 0 ("lead").
+//
+// Arithmetic (restated bit for bit by oracle/fixmodel.c jet_mx): with
+// a~_{i+1} = C_i U_i (C_i = tau/(i+1): the tau-scaled rows of the reference's
+// taylor.py:117 _jet_rows) the numerator of order j = i+1 is linear in U_i
+// apart from the Cauchy sums, which split into the lag-1 terms (rows j-1 and
+// 1) and the rest L'(j) (rows 2..j-2):
+//
+//   U_j   = rnd( sum_j' U_i^j' (x) K_i^{m,j'} + sum_t q_t [lag_t(j) + sum_o split1(P_{o,t}(j))] )
+//   K_i   = rnd( S (x) C_i ),   S^{m,j'} = bnf(lin[m][j'] + sum_t q_t a~_0)     (per step, bulk CTAs)
+//   a~_j  = rnd( U_i (x) C_i )
+//
+// The lead computes, per order, every product of U_i, the new coefficient
+// rows and the lag-1 terms -- one warp per product, all in parallel -- and
+// one rounding per output. The bulk CTAs (ranks 1..G-1, owner of k =
+// 1+(k-1) mod (G-1)) receive each new row from the lead and compute their
+// share of L'(j) two orders ahead, so DSMEM latency and their work are off
+// the critical path. Products are exact int64 column sums (every operand
+// digit is balanced or semi-normal, so no folds are needed), hence the cheap
+// semi-normal rounding (warp_snf_t) is a deterministic function of the
+// inputs and the CPU model reproduces it bit for bit.
+//
+// Work mapping of one product on one warp: the 8-column groups g and
+// ng-1-g are paired (balanced work), each pair's p-range is split evenly over
+// NCH consecutive lanes; a lane runs an 8-column register window (one LDS of
+// A and one of B per 8 IMAD.WIDE); the NCH lanes then reduce-scatter their 16
+// partial columns with shuffles and store exact column sums.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "mpt_common.cuh"
+#include "mpt_device.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace mpt {
+namespace mx {
+
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMacWarps = kWarps - 1;  // warp 15 of the lead gathers L'
+constexpr int kMaxProd = 32;           // products per lead stage
+constexpr int kPerWarpPass = 4;        // bulk products accumulated per lane before a split
+
+struct Geo {
+  int W, KW, T, Tc, ncols, ncp, ng, rs, krs, urs;
+};
+
+__host__ __device__ inline Geo make_geo(const Params& p) {
+  Geo g;
+  g.W = p.W;
+  g.KW = p.W + 1;
+  g.T = p.Lf - 2;
+  g.Tc = p.Lf + p.sc - 2;
+  g.ncols = p.Lf + 4;              // relative columns of every column vector (oracle: ncols)
+  g.ncp = (g.ncols + 3) / 4 * 4;
+  g.ng = (p.Lf + 3 + 7) / 8;       // 8-column groups covering every product column (rel. <= Lf+2)
+  g.rs = (g.KW + 3) / 4 * 4 + kPad;
+  g.krs = (g.KW + 3) / 4 * 4;
+  g.urs = (g.W + 3) / 4 * 4;
+  return g;
+}
+
+__host__ __device__ inline int nch_for(const Geo& g) {
+  const int np = (g.ng + 1) / 2;
+  return np <= 2 ? 16 : np <= 4 ? 8 : np <= 8 ? 4 : 2;
+}
+__host__ __device__ inline int snf_m(int Wout) { return (Wout + 2 + 31) / 32; }
+
+// active entries (m, j) of the K matrix; dyn: depends on the state (bilinear)
+__host__ __device__ inline int n_entries(const Params& p, int* em, int* ej, int* dyn = nullptr) {
+  int n = 0;
+  for (int m = 0; m < p.D; m++)
+    for (int j = 0; j < p.D; j++) {
+      const bool lin = !(p.lin_small[m * p.D + j] && p.lin_int[m * p.D + j] == 0);
+      bool bil = false;
+      for (int t = 0; t < p.NT; t++)
+        if (p.teq[t] == m && (p.pj[p.tpair[t]] == j || p.pk[p.tpair[t]] == j)) bil = true;
+      if (lin || bil) {
+        if (em) em[n] = m;
+        if (ej) ej[n] = j;
+        if (dyn) dyn[n] = bil;
+        n++;
+      }
+    }
+  return n;
+}
+
+struct Layout {
+  int Gb, nE, nslots;
+  size_t off_lrow, off_linfo, off_cpart, off_lsum, off_cbuf, off_recv, off_ssum, lead_total;
+  size_t off_rows, off_rinfo, off_srow, off_sinfo, off_crow, off_cinfo, off_wcol, off_acc, off_bcc, off_kst,
+      off_kcol, bulk_total;
+  size_t total;
+};
+
+// bulk row store: left-hand pair variables for every k, the others for the owned
+// class only. Returns the first slot of variable v (v = -1: total), full[v].
+__host__ __device__ inline int row_slots(const Params& p, int G, int v, int* full) {
+  const int Gb = G - 1;
+  int s = 0;
+  for (int u = 0; u < p.D; u++) {
+    int is_left = 0;
+    for (int q = 0; q < p.NP; q++) is_left |= (p.pj[q] == u);
+    const int f = is_left || Gb <= 1;
+    if (u == v) {
+      if (full) *full = f;
+      return s;
+    }
+    s += f ? p.N + 1 : p.N / (Gb > 0 ? Gb : 1) + 2;
+  }
+  return s;
+}
+
+// lead rows: ST D | SB D | LIN D*D | U 2D | K 2nE | C 2 | ROW 2D | ROW1 D
+__host__ __device__ inline Layout make_layout(const Params& p, int G) {
+  Layout L;
+  const Geo g = make_geo(p);
+  L.Gb = G - 1;
+  L.nE = n_entries(p, nullptr, nullptr);
+  const int NPp = p.NP > 0 ? p.NP : 1;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t r = o;
+    o += (bytes + 15) / 16 * 16;
+    return r;
+  };
+  const int nlrow = 2 * p.D + p.D * p.D + 2 * p.D + 2 * L.nE + 2 + 3 * p.D;
+  L.off_lrow = take(sizeof(int32_t) * ((size_t)nlrow * g.rs + 2 * kPad));
+  L.off_linfo = take(sizeof(int2) * (size_t)nlrow);
+  L.off_cpart = take(sizeof(int64_t) * (size_t)kMaxProd * g.ncp);
+  L.off_lsum = take(sizeof(int64_t) * (size_t)kMaxD * g.ncp);
+  L.off_cbuf = take(sizeof(int64_t) * (size_t)2 * kMaxD * g.ncp);
+  L.off_recv = take(sizeof(int64_t) * 2 * (size_t)(L.Gb > 0 ? L.Gb : 1) * NPp * g.ncp);
+  L.off_ssum = take(sizeof(int64_t) * (size_t)p.D * (g.W + 3));
+  L.lead_total = o;
+  o = 0;
+  L.nslots = row_slots(p, G, -1, nullptr);
+  L.off_rows = take(sizeof(int32_t) * ((size_t)L.nslots * g.rs + 2 * kPad));
+  L.off_rinfo = take(sizeof(int2) * (size_t)L.nslots);
+  L.off_srow = take(sizeof(int32_t) * ((size_t)p.D * p.D * g.rs + 2 * kPad));
+  L.off_sinfo = take(sizeof(int2) * (size_t)p.D * p.D);
+  L.off_crow = take(sizeof(int32_t) * ((size_t)g.rs + 2 * kPad));
+  L.off_cinfo = take(sizeof(int2) * 2);
+  L.off_wcol = take(sizeof(int64_t) * (size_t)kWarps * g.ncp);
+  L.off_acc = take(sizeof(int64_t) * (size_t)NPp * g.ncp);
+  L.off_bcc = take(sizeof(int64_t) * (size_t)NPp * g.ncp);
+  L.off_kst = take(sizeof(int32_t) * (size_t)kWarps * g.krs);
+  L.off_kcol = take(sizeof(int64_t) * (size_t)kWarps * g.ncp);
+  L.bulk_total = o;
+  L.total = L.lead_total > L.bulk_total ? L.lead_total : L.bulk_total;
+  return L;
+}
+
+// ---------------------------------------------------------------------------
+// mbarrier / st.async helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, int n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t par) {
+  asm volatile(
+      "{\n .reg .pred p;\n MXW: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra MXW;\n}" ::"r"(smem_u32(b)),
+      "r"(par)
+      : "memory");
+}
+__device__ __forceinline__ void st_async16(uint32_t raddr, int32_t a, int32_t b, int32_t c, int32_t d, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1,%2,%3,%4}, [%5];" ::"r"(raddr),
+               "r"(a), "r"(b), "r"(c), "r"(d), "r"(rbar)
+               : "memory");
+}
+// one TMA bulk copy from this CTA's shared memory into another CTA's (cluster
+// address from mapa), completing `bytes` on the destination's mbarrier
+__device__ __forceinline__ void bulk_push(uint32_t rdst, uint32_t lsrc, uint32_t bytes, uint32_t rbar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(rdst),
+      "r"(lsrc), "r"(bytes), "r"(rbar)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void cluster_arrive_release() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait_acquire() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_barrier() {
+  cluster_arrive_release();
+  cluster_wait_acquire();
+}
+
+// ---------------------------------------------------------------------------
+// Value-exact balanced digits of V = sum val[c] B^c (oracle bnf_exact): the
+// balanced rounding of col' = (-B/2, 0, val...), i.e. warp_bnf_t below with
+// the rounding half cancelled.
+template <int M>
+__device__ __forceinline__ uint64_t la_carries(uint32_t G, uint32_t P) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const uint32_t allp = (M >= 32) ? 0xffffffffu : ((1u << M) - 1u);
+  auto local = [&](uint32_t cin) -> uint64_t {
+    const uint64_t A = ((uint64_t)G << 1) | cin;
+    const uint64_t S = (A & P) + P;
+    return (S ^ P) | A;
+  };
+  const uint64_t C0 = local(0);
+  const uint32_t Gl = __ballot_sync(full, (C0 >> M) & 1);
+  const uint32_t Pl = __ballot_sync(full, P == allp);
+  const uint64_t A = ((uint64_t)Gl << 1) & 0xffffffffull;
+  const uint64_t S = (A & Pl) + Pl;
+  const uint32_t Cin = ((uint32_t)S ^ Pl) | (uint32_t)A;
+  return local((Cin >> lane) & 1);
+}
+
+// balanced rounding R = floor((V + B^2/2)/B^2) with every digit in [-B/2, B/2)
+// (oracle round_bnf); col[c] for c < ncols, lane l holds columns l*M..l*M+M-1
+template <int M>
+__device__ __noinline__ bool warp_bnf(const int64_t* col, int ncols, int Wout, int32_t* out, int2* info) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  Blk<M> b;
+#pragma unroll
+  for (int j = 0; j < M; j++) {
+    const int c = lane * M + j;
+    b.v[j] = c < ncols ? col[c] : 0;
+    if (c == 1) b.v[j] += kRadix / 2;
+  }
+  int64_t top = blk_rounds(b, M);
+  top += blk_lookahead(b, M, 1);
+  top += blk_lookahead(b, M, -1);
+  const int topc = Wout + 1;
+  bool nz = false, nmax = false;
+#pragma unroll
+  for (int j = 0; j < M; j++) {
+    const int c = lane * M + j;
+    if (c > topc) {
+      nz |= b.v[j] != 0;
+      nmax |= b.v[j] != kMask;
+    }
+  }
+  const bool anynz = __any_sync(full, nz), anynmax = __any_sync(full, nmax);
+  int64_t hi = 0;
+  bool ovf = false;
+  if (!anynz && top == 0)
+    hi = 0;
+  else if (!anynmax && top == -1)
+    hi = -1;
+  else
+    ovf = true;
+  uint32_t G = 0, P = 0;
+#pragma unroll
+  for (int j = 0; j < M; j++) {
+    const int c = lane * M + j;
+    if (c >= 2 && c < topc) {
+      G |= (uint32_t)(b.v[j] >= kRadix / 2) << j;
+      P |= (uint32_t)(b.v[j] == kRadix / 2 - 1) << j;
+    }
+  }
+  const uint64_t C = la_carries<M>(G, P);
+  int bot = 1 << 30, tp = -1;
+#pragma unroll
+  for (int j = 0; j < M; j++) {
+    const int c = lane * M + j;
+    if (c >= 2 && c <= topc) {
+      const int64_t cin = (C >> j) & 1;
+      int64_t e;
+      if (c < topc) {
+        const int64_t cout = ((G >> j) & 1) | (((P >> j) & 1) & cin);
+        e = b.v[j] + cin - kRadix * cout;
+      } else {
+        e = b.v[j] + cin + hi * kRadix;
+        if (e >= kRadix / 2 || e < -(kRadix / 2)) ovf = true;
+      }
+      const int d = c - 2;
+      out[d] = (int32_t)e;
+      if (e) {
+        bot = min(bot, d);
+        tp = max(tp, d);
+      }
+    }
+  }
+  bot = __reduce_min_sync(full, bot);
+  tp = __reduce_max_sync(full, tp);
+  if (lane == 0 && info) *info = make_int2(tp >= 0 ? bot : Wout, tp);
+  const bool any = __any_sync(full, ovf);
+  __syncwarp();
+  return any;
+}
+
+// semi-normal rounding of exact column sums (oracle round_cols), one warp
+template <int M>
+__device__ __noinline__ bool warp_snf_call(const int64_t* col, int ncols, int W, int32_t* out, int2* info) {
+  return warp_snf_t<M>(col, ncols, W, out, info);
+}
+
+__device__ __noinline__ bool warp_canon(const int64_t* col, int ncols, int W, int32_t* out, int2* info, int prec) {
+  return warp_normalize(col, ncols, 0, W, out, info, prec);
+}
+
+// ---------------------------------------------------------------------------
+// exact products on one warp
+
+// s64 += s32 * s32 as one IMAD.WIDE (the C++ form lets nvcc split it into
+// IMAD.WIDE.U32 + sign corrections)
+__device__ __forceinline__ int64_t madw(int32_t a, int32_t b, int64_t c) {
+  int64_t d;
+  asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+  return d;
+}
+// shared-memory accesses by 32-bit address (used inside the out-of-line product
+// routine, where the data is stable for the whole call)
+__device__ __forceinline__ int32_t lds32(uint32_t a) {
+  int32_t v;
+  asm("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int64_t lds64(uint32_t a) {
+  int64_t v;
+  asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts64(uint32_t a, int64_t v) {
+  asm volatile("st.shared.b64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+
+// one masked block of 8 p-steps: acc[r] += sum_{p in [p0, min(p0+7, p1)]} A[p] B[c0+r-p];
+// straight-line code (8 loads of A, 15 of B, 64 IMAD.WIDE). Rows are zero-padded
+// by kPad digits, so the reads past the ranges are harmless.
+__device__ __forceinline__ void mac_block(int64_t (&acc)[8], uint32_t A, uint32_t B, int c0, int p0, int p1) {
+  int32_t a[8], b[15];
+#pragma unroll
+  for (int u = 0; u < 8; u++) a[u] = (p0 + u <= p1) ? lds32(A + 4 * (p0 + u)) : 0;
+#pragma unroll
+  for (int t = 0; t < 15; t++) b[t] = lds32(B + 4 * (c0 - p0 - 7 + t));
+#pragma unroll
+  for (int u = 0; u < 8; u++)
+#pragma unroll
+    for (int r = 0; r < 8; r++) acc[r] = madw(a[u], b[r - u + 7], acc[r]);
+}
+
+// useful digit products of group [c0, c0+8) for nonzero ranges ia, ib (counters only)
+__device__ __forceinline__ unsigned long long group_macs(int2 ia, int2 ib, int c0) {
+  unsigned long long n = 0;
+  for (int r = 0; r < 8; r++) {
+    const int c = c0 + r;
+    const int lo = max(ia.x, c - ib.y), hi = min(ia.y, c - ib.x);
+    if (hi >= lo) n += hi - lo + 1;
+  }
+  return n;
+}
+
+// A product for the out-of-line warp routine: shared addresses of digit 0 of
+// both rows and their nonzero ranges.
+struct Prod {
+  uint32_t A, B;
+  int2 ia, ib;
+};
+
+// One warp: sum_k A_k (x) B_k (truncation T, relative column c - T), nprod <=
+// 4 products accumulated exactly in the lanes' registers, then the NCH lanes
+// of each group pair reduce-scatter and the exact columns are stored to
+// `out` (shared address of int64[nout+...]): overwritten (zero-filled first)
+// or accumulated. Group pairs (g, ng-1-g) balance the triangle; blocks of 8
+// p-steps are dealt round-robin to the pair's lanes. ONE out-of-line copy of
+// this code serves every product of the kernel (instruction-cache footprint).
+template <int NCH>
+__device__ __noinline__ void warp_prods(const Prod* desc, int nprod, int T, int ng, uint32_t out, int ncp, int nout,
+                                        int accumulate, MacCount* mc) {
+  const int lane = threadIdx.x & 31;
+  const int gp = lane / NCH, ch = lane % NCH;
+  const int npair = (ng + 1) / 2;
+  const int g1 = gp, g2 = ng - 1 - gp;
+  const int c01 = T + 8 * g1, c02 = T + 8 * g2;
+  int64_t a1[8], a2[8];
+#pragma unroll
+  for (int r = 0; r < 8; r++) a1[r] = a2[r] = 0;
+#pragma unroll 1
+  for (int k = 0; k < nprod; k++) {
+    const Prod P = desc[k];
+    if (gp >= npair || P.ia.y < 0 || P.ib.y < 0) continue;
+    const int lo1 = max(P.ia.x, c01 - P.ib.y), hi1 = min(P.ia.y, c01 + 7 - P.ib.x);
+    const int nb1 = hi1 >= lo1 ? (hi1 - lo1 + 8) / 8 : 0;
+    int lo2 = 0, hi2 = -1, nb2 = 0;
+    if (g2 > g1) {
+      lo2 = max(P.ia.x, c02 - P.ib.y);
+      hi2 = min(P.ia.y, c02 + 7 - P.ib.x);
+      nb2 = hi2 >= lo2 ? (hi2 - lo2 + 8) / 8 : 0;
+    }
+#pragma unroll 1
+    for (int b = ch; b < nb1 + nb2; b += NCH) {
+      int64_t t[8];
+      const bool first = b < nb1;
+#pragma unroll
+      for (int r = 0; r < 8; r++) t[r] = 0;
+      mac_block(t, P.A, P.B, first ? c01 : c02, first ? lo1 + 8 * b : lo2 + 8 * (b - nb1), first ? hi1 : hi2);
+#pragma unroll
+      for (int r = 0; r < 8; r++) {
+        a1[r] += first ? t[r] : 0;
+        a2[r] += first ? 0 : t[r];
+      }
+    }
+    if (mc && ch == 0) {
+      mc->useful += group_macs(P.ia, P.ib, c01) + (g2 > g1 ? group_macs(P.ia, P.ib, c02) : 0);
+      mc->executed += 64ull * (nb1 + nb2);
+    }
+  }
+  if (!accumulate)
+    for (int c = lane; c < ncp; c += 32) sts64(out + 8 * c, 0);
+  __syncwarp();
+  // reduce-scatter over the NCH lanes of each pair
+  int64_t v[16];
+#pragma unroll
+  for (int r = 0; r < 8; r++) {
+    v[r] = a1[r];
+    v[8 + r] = a2[r];
+  }
+  int base = 0;
+#pragma unroll
+  for (int s = NCH / 2, n = 16; s >= 1; s >>= 1, n >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      if (j < n / 2) {
+        const int64_t send = up ? v[j] : v[n / 2 + j];
+        const int64_t keep = up ? v[n / 2 + j] : v[j];
+        v[j] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+      }
+    }
+    if (up) base += n / 2;
+  }
+  if (gp < npair) {
+    constexpr int nf = 16 / NCH;
+#pragma unroll
+    for (int j = 0; j < nf; j++) {
+      const int idx = base + j;
+      const int g = idx < 8 ? g1 : g2;
+      if (idx >= 8 && g2 <= g1) continue;
+      const int rel = 8 * g + (idx & 7);
+      if (rel < nout) {
+        const uint32_t a = out + 8 * rel;
+        sts64(a, accumulate ? lds64(a) + v[j] : v[j]);
+      }
+    }
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ Prod mkprod(const int32_t* A, int2 ia, const int32_t* B, int2 ib) {
+  return Prod{smem_u32(A), smem_u32(B), ia, ib};
+}
+
+// one product, columns overwritten; `slot` = this warp's descriptor slot (shared)
+template <int NCH>
+__device__ __forceinline__ void warp_product(Prod* slot, const int32_t* A, int2 ia, const int32_t* B, int2 ib, int T,
+                                             const Geo& g, int64_t* out, MacCount* mc) {
+  if ((threadIdx.x & 31) == 0) slot[0] = mkprod(A, ia, B, ib);
+  __syncwarp();
+  warp_prods<NCH>(slot, 1, T, g.ng, smem_u32(out), g.ncp, g.ncols, 0, mc);
+}
+
+__device__ __forceinline__ int2 row_info(const int32_t* r, int n) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  int bot = 1 << 30, tp = -1;
+  for (int d = lane; d < n; d += 32)
+    if (r[d]) {
+      bot = min(bot, d);
+      tp = max(tp, d);
+    }
+  bot = __reduce_min_sync(full, bot);
+  tp = __reduce_max_sync(full, tp);
+  return make_int2(tp >= 0 ? bot : n, tp);
+}
+
+// ---------------------------------------------------------------------------
+template <int NPT, int NCH, int MS, int MK>
+__global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_constant__ Params p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ __align__(8) uint64_t s_bar[4];
+  __shared__ int s_flag;
+  __shared__ int s_em[kMaxD * kMaxD], s_ej[kMaxD * kMaxD], s_dyn[kMaxD * kMaxD];
+  __shared__ int s_base[kMaxD], s_full[kMaxD];
+  __shared__ Prod s_prod[kWarps][kPerWarpPass];
+  __shared__ int s_wq[kWarps];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int G = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int traj = blockIdx.x / G;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Geo g = make_geo(p);
+  const Layout L = make_layout(p, G);
+  const int Gb = L.Gb;
+  const int nE = L.nE;
+  const int NPp = p.NP > 0 ? p.NP : 1;
+  const int N = p.N;
+  MacCount mcount;
+  MacCount* mc = p.counters ? &mcount : nullptr;
+  int32_t* ktab = (int32_t*)p.gscratch + (size_t)traj * N * nE * g.krs;
+  int2* kinfo = (int2*)((int32_t*)p.gscratch + (size_t)p.n_traj * N * nE * g.krs) + (size_t)traj * N * nE;
+  int32_t* gstate = p.state + (size_t)traj * p.D * p.RS;
+
+  for (size_t w = tid; w < L.total / 4; w += kThreads) ((int32_t*)smem)[w] = 0;
+  if (tid == 0) {
+    n_entries(p, s_em, s_ej, s_dyn);
+    s_flag = 0;
+    for (int b = 0; b < 4; b++) mbar_init(&s_bar[b], 1);
+  }
+  if (tid < kMaxD) {
+    int f = 1;
+    s_base[tid] = tid < p.D ? row_slots(p, G, tid, &f) : 0;
+    s_full[tid] = f;
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  const int R_ST = 0, R_SB = p.D, R_LIN = 2 * p.D, R_U = R_LIN + p.D * p.D, R_K = R_U + 2 * p.D,
+            R_C = R_K + 2 * nE, R_ROW = R_C + 2, R_ROW1 = R_ROW + 2 * p.D;
+  if (rank == 0) {
+    int32_t* lrow = (int32_t*)(smem + L.off_lrow) + kPad;
+    for (int r = 0; r < p.D * p.D; r++)
+      for (int d = tid; d < p.W; d += kThreads) lrow[(size_t)(R_LIN + r) * g.rs + d] = p.lin[(size_t)r * p.RS + d];
+    for (int m = 0; m < p.D; m++)
+      for (int d = tid; d < p.W; d += kThreads) lrow[(size_t)(R_ST + m) * g.rs + d] = gstate[(size_t)m * p.RS + d];
+  }
+  __syncthreads();
+  cluster.sync();
+
+  const uint32_t row_bytes = (uint32_t)(g.urs * 4);  // one row (bulk copy)
+  const uint32_t recv_bytes = (uint32_t)(Gb * NPp * g.ncp * 8);
+  const uint32_t bar_local = smem_u32(&s_bar[0]);
+  auto owner = [&](int k) { return 1 + (k - 1) % Gb; };
+  auto SLOT = [&](int v, int k) { return s_base[v] + (s_full[v] ? k : k / Gb); };
+
+  if (rank == 0) {
+    // =============================== lead ===============================
+    int32_t* lrow = (int32_t*)(smem + L.off_lrow) + kPad;
+    int2* linfo = (int2*)(smem + L.off_linfo);
+    int64_t* cpart = (int64_t*)(smem + L.off_cpart);
+    int64_t* lsum = (int64_t*)(smem + L.off_lsum);
+    int64_t* cbuf = (int64_t*)(smem + L.off_cbuf);
+    int64_t* recv = (int64_t*)(smem + L.off_recv);
+    int64_t* ssum = (int64_t*)(smem + L.off_ssum);
+    auto LR = [&](int r) { return lrow + (size_t)r * g.rs; };
+    const uint32_t rows_remote = smem_u32(smem + L.off_rows) + 4 * kPad;
+    for (int r = warp; r < R_U; r += kWarps) {
+      if (r >= R_SB && r < R_LIN) continue;
+      const int2 inf = row_info(LR(r), p.W);
+      if (lane == 0) linfo[r] = inf;
+    }
+    __syncthreads();
+    uint32_t rph = 0;
+
+    // lane 0 of a row warp: push new row m (index r, lead buffer `src`) to the bulk CTAs that keep it
+    auto push_row = [&](int m, int r, const int32_t* src) {
+      const int sl = SLOT(m, r);
+      const uint32_t rb_local = bar_local + 8 * (r & 3);
+      fence_async_smem();
+      for (int dst = 1; dst < G; dst++) {
+        if (!s_full[m] && dst != owner(r)) continue;
+        bulk_push(mapa_u32(rows_remote + 4 * sl * g.rs, dst), smem_u32(src), (uint32_t)(g.urs * 4), mapa_u32(rb_local, dst));
+      }
+      bulk_commit();
+    };
+    // C_i into buffer b (cp.async, 16-byte chunks; ctab rows are RS-strided, RS >= W, multiple of 4)
+    auto prefetch_c = [&](int i, int b) {
+      if (warp == kWarps - 1) {
+        const int32_t* src = p.ctab + (size_t)i * p.RS;
+        int32_t* dst = LR(R_C + b);
+        for (int c = lane; c < p.RS / 4; c += 32)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + 4 * c)), "l"(src + 4 * c)
+                       : "memory");
+      }
+    };
+    auto prefetch_k = [&](int i, int b) {
+      for (int e = warp; e < nE; e += kWarps) {
+        const int32_t* src = ktab + ((size_t)i * nE + e) * g.krs;
+        int32_t* dst = LR(R_K + b * nE + e);
+        for (int c = lane; c < g.krs / 4; c += 32)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + 4 * c)), "l"(src + 4 * c)
+                       : "memory");
+        if (lane == 0) linfo[R_K + b * nE + e] = __ldcg(kinfo + (size_t)i * nE + e);
+      }
+    };
+
+    for (int n = p.start_step + 1; n <= p.n_steps; n++) {
+      // ---- step start: row 0 = state (ssum), SB = bnf(state), U_0
+      for (int m = 0; m < p.D; m++)
+        for (int d = tid; d < p.W + 3; d += kThreads) ssum[(size_t)m * (p.W + 3) + d] = d < p.W ? LR(R_ST + m)[d] : 0;
+      if (p.write_coef)
+        for (int m = 0; m < p.D; m++)
+          for (int d = tid; d < p.W; d += kThreads)
+            p.coef[(((size_t)traj * p.D + m) * (N + 1)) * p.RS + d] = LR(R_ST + m)[d];
+      if (warp < p.D) {  // SB_m = bnf(state_m)
+        int64_t* cv = cbuf + (size_t)warp * g.ncp;
+        for (int c = lane; c < g.ncp; c += 32) cv[c] = c == 0 ? -(kRadix / 2) : (c >= 2 && c - 2 < p.W ? LR(R_ST + warp)[c - 2] : 0);
+        __syncwarp();
+        if (warp_bnf<MS>(cv, g.ncols, p.W, LR(R_SB + warp), &linfo[R_SB + warp]) && lane == 0) atomicOr(&s_flag, 1);
+      }
+      __syncthreads();
+      {
+        // products: lin[m][j] (x) SB_j, q_t SB_a (x) SB_b
+        int np = 0;
+        for (int m = 0; m < p.D; m++)
+          for (int j = 0; j < p.D; j++) {
+            const int r = R_LIN + m * p.D + j;
+            if (linfo[r].y < 0) continue;
+            if (np % kWarps == warp)
+              warp_product<NCH>(s_prod[warp], LR(r), linfo[r], LR(R_SB + j), linfo[R_SB + j], g.T, g, cpart + (size_t)np * g.ncp, mc);
+            np++;
+          }
+        for (int t = 0; t < p.NT; t++) {
+          const int a = p.pj[p.tpair[t]], b = p.pk[p.tpair[t]];
+          if (np % kWarps == warp)
+            warp_product<NCH>(s_prod[warp], LR(R_SB + a), linfo[R_SB + a], LR(R_SB + b), linfo[R_SB + b], g.T, g,
+                              cpart + (size_t)np * g.ncp, mc);
+          np++;
+        }
+        __syncthreads();
+        if (warp < p.D) {
+          const int m = warp;
+          int64_t* cv = cbuf + (size_t)m * g.ncp;
+          for (int c = lane; c < g.ncols; c += 32) {
+            int64_t s = 0;
+            int k = 0;
+            for (int mm = 0; mm < p.D; mm++)
+              for (int j = 0; j < p.D; j++) {
+                if (linfo[R_LIN + mm * p.D + j].y < 0) continue;
+                if (mm == m) s += cpart[(size_t)k * g.ncp + c];
+                k++;
+              }
+            for (int t = 0; t < p.NT; t++, k++)
+              if (p.teq[t] == m) s += (int64_t)p.tq_int[t] * cpart[(size_t)k * g.ncp + c];
+            if (c >= 2 && c - 2 < p.W) s += p.cst[(size_t)m * p.RS + c - 2];
+            cv[c] = s;
+          }
+          __syncwarp();
+          if (warp_snf_call<MS>(cv, g.ncols, p.W, LR(R_U + m), &linfo[R_U + m]) && lane == 0) atomicOr(&s_flag, 1);
+        }
+      }
+      prefetch_c(0, 0);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      __syncthreads();
+      cluster_barrier();  // [C] the K table of this step is complete
+      if (N >= 2) prefetch_k(0, 0);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncthreads();
+      if (warp == 0) {
+        const int2 inf = row_info(LR(R_C + 0), p.W);
+        if (lane == 0) linfo[R_C + 0] = inf;
+      }
+      __syncthreads();
+
+      for (int i = 0; i < N; i++) {
+        const int par = i & 1, j = i + 1;
+        const bool tlog = p.dbg && n == p.start_step + 1 && i < 64 && lane == 0;
+#define LT(k) \
+  if (tlog) p.dbg[((size_t)i * 16 + warp) * 8 + (k)] = (long long)clock64();
+        LT(0);
+        const bool doU = j <= N - 1;
+        const int lagn = (j >= 2 && j <= N - 1) ? (j == 2 ? 1 : 2) : 0;
+        const int nEu = doU ? nE : 0;
+        const int P = nEu + p.D + p.NT * lagn;
+        // prefetch C_{i+1}, K_{i+1} (their buffers were last read at order i-1)
+        if (i + 1 < N) prefetch_c(i + 1, par ^ 1);
+        if (i + 2 < N) prefetch_k(i + 1, par ^ 1);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        if (warp < kMacWarps) {
+#pragma unroll 1
+          for (int pi = warp; pi < P; pi += kMacWarps) {
+            const int32_t *A, *B;
+            int2 ia, ib;
+            int T = g.Tc;
+            if (pi < nEu) {
+              A = LR(R_U + par * p.D + s_ej[pi]);
+              ia = linfo[R_U + par * p.D + s_ej[pi]];
+              B = LR(R_K + par * nE + pi);
+              ib = linfo[R_K + par * nE + pi];
+            } else if (pi < nEu + p.D) {
+              const int m = pi - nEu;
+              A = LR(R_U + par * p.D + m);
+              ia = linfo[R_U + par * p.D + m];
+              B = LR(R_C + par);
+              ib = linfo[R_C + par];
+            } else {
+              const int l = pi - nEu - p.D, t = l / lagn, side = l - t * lagn;
+              const int a = p.pj[p.tpair[t]], b = p.pk[p.tpair[t]];
+              const int ra = (lagn == 2 && side == 0) ? R_ROW + par * p.D + a : R_ROW1 + a;
+              const int rb = (lagn == 2 && side == 1) ? R_ROW + par * p.D + b : R_ROW1 + b;
+              A = LR(ra);
+              ia = linfo[ra];
+              B = LR(rb);
+              ib = linfo[rb];
+              T = g.T;
+            }
+            warp_product<NCH>(s_prod[warp], A, ia, B, ib, T, g, cpart + (size_t)pi * g.ncp, mc);
+          }
+        } else {
+          // aux warp: q_t * sum of the bulk CTAs' L'(j) into lsum[m]
+          const bool have = doU && j >= 4 && p.NP > 0;
+          if (have) {
+            const int rp = j & 1;
+            if (lane == 0) mbar_expect(&s_bar[rp], recv_bytes);
+            mbar_wait(&s_bar[rp], (rph >> rp) & 1);
+            rph ^= 1u << rp;
+          }
+          const int64_t* rv = recv + (size_t)(j & 1) * Gb * NPp * g.ncp;
+          for (int m = 0; m < p.D; m++)
+            for (int c = lane; c < g.ncols; c += 32) {
+              int64_t s = 0;
+              if (have)
+                for (int t = 0; t < p.NT; t++) {
+                  if (p.teq[t] != m) continue;
+                  const int q = p.tpair[t];
+                  int64_t v = 0;
+                  for (int r = 0; r < Gb; r++) v += rv[((size_t)r * NPp + q) * g.ncp + c];
+                  s += (int64_t)p.tq_int[t] * v;
+                }
+              lsum[(size_t)m * g.ncp + c] = s;
+            }
+        }
+        LT(1);
+        __syncthreads();
+        LT(2);
+        // ---- roundings: U_{j}^m (warps 0..D-1), rows a~_{i+1}^m (warps D..2D-1)
+        if (warp < 2 * p.D) {
+          const bool isU = warp < p.D;
+          const int m = isU ? warp : warp - p.D;
+          if (!isU || doU) {
+            int64_t* cv = cbuf + (size_t)warp * g.ncp;
+            for (int c = lane; c < g.ncols; c += 32) {
+              int64_t s;
+              if (isU) {
+                s = lsum[(size_t)m * g.ncp + c];
+                for (int e = 0; e < nE; e++)
+                  if (s_em[e] == m) s += cpart[(size_t)e * g.ncp + c];
+                for (int l = 0; l < p.NT * lagn; l++) {
+                  const int t = l / lagn;
+                  if (p.teq[t] == m) s += (int64_t)p.tq_int[t] * cpart[(size_t)(nEu + p.D + l) * g.ncp + c];
+                }
+              } else {
+                s = cpart[(size_t)(nEu + m) * g.ncp + c];
+              }
+              cv[c] = s;
+            }
+            __syncwarp();
+            if (isU) {
+              if (warp_snf_call<MS>(cv, g.ncols, p.W, LR(R_U + (par ^ 1) * p.D + m), &linfo[R_U + (par ^ 1) * p.D + m]) &&
+                  lane == 0)
+                atomicOr(&s_flag, 1);
+            } else {
+              const int rr = R_ROW + (par ^ 1) * p.D + m;
+              if (lane == 0) bulk_wait_read();  // the copies of row i-1 (same buffer) have read it
+              __syncwarp();
+              if (warp_snf_call<MS>(cv, g.ncols, p.W, LR(rr), &linfo[rr]) && lane == 0) atomicOr(&s_flag, 1);
+              __syncwarp();
+              for (int d = lane; d < p.W; d += 32) ssum[(size_t)m * (p.W + 3) + d] += LR(rr)[d];
+              if (i == 0) {
+                for (int d = lane; d < p.W; d += 32) LR(R_ROW1 + m)[d] = LR(rr)[d];
+                if (lane == 0) linfo[R_ROW1 + m] = linfo[rr];
+              }
+              if (p.write_coef)
+                for (int d = lane; d < p.W; d += 32)
+                  p.coef[(((size_t)traj * p.D + m) * (N + 1) + j) * p.RS + d] = LR(rr)[d];
+              __syncwarp();
+              if (lane == 0) push_row(m, j, LR(rr));
+            }
+          }
+        }
+        LT(3);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        LT(4);
+        __syncthreads();
+        LT(5);
+        if (i + 1 < N && warp == 0) {
+          const int2 inf = row_info(LR(R_C + (par ^ 1)), p.W);
+          if (lane == 0) linfo[R_C + (par ^ 1)] = inf;
+        }
+        __syncthreads();
+        LT(6);
+#undef LT
+      }
+      // ---- end of step: state = RN_P(sum of rows)
+      if (warp < p.D) {
+        const int m = warp;
+        if (warp_canon(ssum + (size_t)m * (p.W + 3), p.W + 3, p.W, LR(R_ST + m), &linfo[R_ST + m], p.P) && lane == 0)
+          atomicOr(&s_flag, 1);
+        if ((n % p.stride == 0) || (n == p.n_steps)) {
+          const int slot = (n % p.stride == 0) ? (n / p.stride - p.start_step / p.stride)
+                                               : (p.n_steps / p.stride - p.start_step / p.stride + 1);
+          int32_t* dst = p.rec + ((size_t)slot * p.n_traj + traj) * p.D * p.RS + (size_t)m * p.RS;
+          for (int d = lane; d < p.W; d += 32) dst[d] = LR(R_ST + m)[d];
+        }
+      }
+      __syncthreads();
+      cluster_barrier();  // [B] the new state is visible to the bulk CTAs
+    }
+    for (int m = 0; m < p.D; m++)
+      for (int d = tid; d < p.W; d += kThreads) gstate[(size_t)m * p.RS + d] = LR(R_ST + m)[d];
+  } else {
+    // =============================== bulk ===============================
+    const int o = rank;
+    int32_t* rows = (int32_t*)(smem + L.off_rows) + kPad;
+    int2* rinfo = (int2*)(smem + L.off_rinfo);
+    int32_t* srow = (int32_t*)(smem + L.off_srow) + kPad;
+    int2* sinfo = (int2*)(smem + L.off_sinfo);
+    int32_t* crow = (int32_t*)(smem + L.off_crow) + kPad;
+    int2* cinfo = (int2*)(smem + L.off_cinfo);
+    int64_t* wcol = (int64_t*)(smem + L.off_wcol);
+    int64_t* accA = (int64_t*)(smem + L.off_acc);
+    int64_t* accB = (int64_t*)(smem + L.off_bcc);
+    int32_t* kst = (int32_t*)(smem + L.off_kst);
+    int64_t* kcol = (int64_t*)(smem + L.off_kcol);
+    auto ROW = [&](int v, int k) { return rows + (size_t)SLOT(v, k) * g.rs; };
+    auto RINF = [&](int v, int k) { return rinfo[SLOT(v, k)]; };
+    const uint32_t recv_remote = smem_u32(smem + L.off_recv);
+    const int32_t* lead_state = cluster.map_shared_rank((int32_t*)(smem + L.off_lrow) + kPad, 0);
+    uint32_t rph4 = 0;  // phase bits of the 4 row barriers
+    int nfull = 0;
+    for (int v = 0; v < p.D; v++) nfull += s_full[v];
+
+    // exact per-CTA accumulation: every warp's exact partial columns -> (A, B) = (sum of low digits, sum of carries)
+    auto absorb = [&](int nw_used) {
+      __syncthreads();
+      for (int e = tid; e < p.NP * g.ncols; e += kThreads) {
+        const int q = e / g.ncols, c = e - q * g.ncols;
+        int64_t a = 0, b = 0;
+        for (int w = 0; w < nw_used; w++)
+          if (s_wq[w] == q) {
+            const int64_t v = wcol[(size_t)w * g.ncp + c];
+            a += v & kMask;
+            b += v >> kRadixBits;
+          }
+        accA[(size_t)q * g.ncp + c] += a;
+        accB[(size_t)q * g.ncp + c] += b;
+      }
+      __syncthreads();
+    };
+
+    for (int n = p.start_step + 1; n <= p.n_steps; n++) {
+      const bool first = n == p.start_step + 1;
+      if (tid == 0) bulk_wait_read();  // the last push of the previous step has read the staging area
+      __syncthreads();
+      // ---- S^e = bnf(lin + q state) (exact)
+      for (int e = tid; e < NPp * g.ncp; e += kThreads) accA[e] = accB[e] = 0;
+      if (warp < nE) {
+        const int e = warp, m = s_em[e], j = s_ej[e];
+        int64_t* cv = kcol + (size_t)e * g.ncp;
+        for (int c = lane; c < g.ncp; c += 32) {
+          int64_t s = 0;
+          if (c == 0) s = -(kRadix / 2);
+          if (c >= 2 && c - 2 < p.W) {
+            const int d = c - 2;
+            s = p.lin[(size_t)(m * p.D + j) * p.RS + d];
+            for (int t = 0; t < p.NT; t++) {
+              if (p.teq[t] != m) continue;
+              const int a = p.pj[p.tpair[t]], b = p.pk[p.tpair[t]];
+              if (a == j) s += (int64_t)p.tq_int[t] * lead_state[(size_t)b * g.rs + d];
+              if (b == j) s += (int64_t)p.tq_int[t] * lead_state[(size_t)a * g.rs + d];
+            }
+          }
+          cv[c] = s;
+        }
+        __syncwarp();
+        if (warp_bnf<MS>(cv, g.ncols, p.W, srow + (size_t)e * g.rs, &sinfo[e]) && lane == 0) atomicOr(&s_flag, 1);
+      }
+      __syncthreads();
+      // ---- K_i^e = rnd_{KW}(S^e (x) C_i), i = o-1, o-1+Gb, ... < N-1; state-free entries only once
+      for (int i = o - 1; i + 1 < N; i += Gb) {
+        for (int d = tid; d < p.W; d += kThreads) crow[d] = __ldg(p.ctab + (size_t)i * p.RS + d);
+        __syncthreads();
+        if (warp == 0) {
+          const int2 inf = row_info(crow, p.W);
+          if (lane == 0) cinfo[0] = inf;
+        }
+        __syncthreads();
+        for (int e = warp; e < nE; e += kWarps) {
+          if (!first && !s_dyn[e]) continue;
+          int64_t* cv = kcol + (size_t)warp * g.ncp;
+          warp_product<NCH>(s_prod[warp], srow + (size_t)e * g.rs, sinfo[e], crow, cinfo[0], g.T, g, cv, mc);
+          int2 inf;
+          int32_t* out = kst + (size_t)warp * g.krs;
+          if (warp_snf_call<MK>(cv, g.ncols, g.KW, out, &inf) && lane == 0) atomicOr(&s_flag, 1);
+          __syncwarp();
+          int32_t* dst = ktab + ((size_t)i * nE + e) * g.krs;
+          for (int d = lane; d < g.krs; d += 32) dst[d] = d < g.KW ? out[d] : 0;
+          if (lane == 0) kinfo[(size_t)i * nE + e] = inf;
+        }
+        __syncthreads();
+      }
+      cluster_barrier();  // [C]
+
+      for (int r = 1; r <= N; r++) {
+        const bool own = owner(r) == o;
+        const int rb = r & 3;
+        if (tid == 0) mbar_expect(&s_bar[rb], row_bytes * (uint32_t)(own ? p.D : nfull));
+        mbar_wait(&s_bar[rb], (rph4 >> rb) & 1);
+        rph4 ^= 1u << rb;
+        if (warp < p.D && (own || s_full[warp])) {  // nonzero ranges of the rows that arrived
+          const int2 inf = row_info(ROW(warp, r), p.W);
+          if (lane == 0) rinfo[SLOT(warp, r)] = inf;
+        }
+        __syncthreads();
+        // (a) new terms of L'(r+2): k = 2 (rows r, 2) in owner(2); k = r (rows 2, r) in owner(r), r != 2
+        if (r >= 2 && r + 2 <= N - 1 && p.NP > 0) {
+          int nw = 0;
+          for (int q = 0; q < p.NP; q++) {
+            const int a = p.pj[q], b = p.pk[q];
+            if (owner(2) == o) {
+              if (nw == warp)
+                warp_product<NCH>(s_prod[warp], ROW(a, r), RINF(a, r), ROW(b, 2), RINF(b, 2), g.T, g, wcol + (size_t)nw * g.ncp, mc);
+              if (tid == 0) s_wq[nw] = q;
+              nw++;
+            }
+            if (r != 2 && own) {
+              if (nw == warp)
+                warp_product<NCH>(s_prod[warp], ROW(a, 2), RINF(a, 2), ROW(b, r), RINF(b, r), g.T, g, wcol + (size_t)nw * g.ncp, mc);
+              if (tid == 0) s_wq[nw] = q;
+              nw++;
+            }
+          }
+          if (nw > 0) absorb(nw);
+        }
+        // (b) push split1(P_o) of L'(r+2) to the lead
+        if (r + 2 >= 4 && r + 2 <= N - 1 && p.NP > 0) {
+          const int j = r + 2;
+          int64_t* stg = kcol;  // staging of this CTA's split1(P_o): [q][c]
+          if (tid == 0) bulk_wait_read();  // the previous push has read the staging buffer
+          __syncthreads();
+          for (int e = tid; e < p.NP * g.ncp; e += kThreads) {
+            const int q = e / g.ncp, c = e - q * g.ncp;
+            int64_t x = 0;
+            if (c < g.ncols) {
+              x = accA[(size_t)q * g.ncp + c] & kMask;
+              if (c >= 1) x += (accA[(size_t)q * g.ncp + c - 1] >> kRadixBits) + accB[(size_t)q * g.ncp + c - 1];
+            }
+            stg[e] = x;
+          }
+          __syncthreads();
+          if (tid == 0) {
+            fence_async_smem();
+            const uint32_t off = (uint32_t)((((size_t)(j & 1) * Gb + (o - 1)) * NPp) * g.ncp * 8);
+            bulk_push(mapa_u32(recv_remote + off, 0), smem_u32(stg), (uint32_t)(p.NP * g.ncp * 8),
+                      mapa_u32(bar_local + 8 * (j & 1), 0));
+            bulk_commit();
+          }
+          __syncthreads();
+          for (int e = tid; e < NPp * g.ncp; e += kThreads) accA[e] = accB[e] = 0;
+          __syncthreads();
+        }
+        // (c) old terms of L'(r+3): k in [3, r] owned, rows r+3-k and k
+        if (r + 3 <= N - 1 && r >= 3 && p.NP > 0) {
+          int kfirst = 3;
+          while (owner(kfirst) != o) kfirst++;
+          const int nk = kfirst <= r ? (r - kfirst) / Gb + 1 : 0;
+          const int nprod = nk * p.NP;
+          // warps take products round-robin by pair: warp w -> pair w % NP, k index w / NP (+ stride)
+          const int wpp = kWarps / p.NP;  // warps per pair
+          for (int base = 0; base < nk; base += wpp * kPerWarpPass) {
+            if (tid < kWarps) s_wq[tid] = (tid < wpp * p.NP) ? tid % p.NP : -1;
+            if (warp < wpp * p.NP) {
+              const int q = warp % p.NP, kw = warp / p.NP;
+              const int a = p.pj[q], b = p.pk[q];
+              int np = 0;
+              for (int u = 0; u < kPerWarpPass; u++) {
+                const int kk = base + kw + u * wpp;
+                if (kk >= nk) break;
+                const int k = kfirst + kk * Gb;
+                if (lane == 0) s_prod[warp][u] = mkprod(ROW(a, r + 3 - k), RINF(a, r + 3 - k), ROW(b, k), RINF(b, k));
+                np = u + 1;
+              }
+              __syncwarp();
+              warp_prods<NCH>(s_prod[warp], np, g.T, g.ng, smem_u32(wcol + (size_t)warp * g.ncp), g.ncp, g.ncols, 0, mc);
+            }
+            absorb(kWarps);
+          }
+          (void)nprod;
+        }
+      }
+      cluster_barrier();  // [B]
+    }
+  }
+  bulk_wait_read();  // bulk copies issued by this thread have read their sources
+  __syncthreads();
+  cluster.sync();
+  if (rank != 0 && tid == 0 && (s_flag & 1)) {
+    int* lead_flag = cluster.map_shared_rank(&s_flag, 0);
+    atomicOr(lead_flag, 1);
+  }
+  cluster.sync();
+  if (rank == 0 && tid == 0) p.status[traj] = (s_flag & 1) ? kOverflow : kOk;
+  if (mc) {
+    atomicAdd(&p.counters[0], mcount.useful);
+    atomicAdd(&p.counters[1], mcount.executed);
+  }
+}
+
+}  // namespace mx
+
+size_t mx_smem_bytes(const Params& p, int G) { return mx::make_layout(p, G).total; }
+
+size_t mx_scratch_bytes(const Params& p) {
+  const mx::Geo g = mx::make_geo(p);
+  const int nE = mx::n_entries(p, nullptr, nullptr);
+  return (size_t)p.n_traj * p.N * nE * (g.krs * 4 + 8);
+}
+
+bool mx_supported(const Params& p) {
+  const mx::Geo g = mx::make_geo(p);
+  int em[kMaxD * kMaxD], ej[kMaxD * kMaxD];
+  const int nE = mx::n_entries(p, em, ej);
+  // exact int64 column sums on the lead: products per U target x (W 2^54 + 2^56) < 2^63
+  int worst = 0;
+  for (int m = 0; m < p.D; m++) {
+    int c = 0;
+    for (int e = 0; e < nE; e++) c += em[e] == m;
+    for (int t = 0; t < p.NT; t++) c += 2 * (p.teq[t] == m);
+    worst = c > worst ? c : worst;
+  }
+  const double bound = (double)worst * ((double)p.W * 18014398509481984.0 + 72057594037927936.0);
+  const int nlag = 2 * p.NT;
+  return p.D <= kMaxD && p.all_q_small && p.NP >= 1 && p.NP <= 4 && nE + p.D + nlag <= mx::kMaxProd &&
+         2 * p.D <= mx::kWarps && nE <= mx::kWarps && g.W <= 120 && bound < 9.0e18 &&
+         mx::kWarps / p.NP >= 1 && mx::snf_m(g.KW) <= 4;
+}
+
+template <int NPT, int NCH>
+static const void* mx_fn_ms(int ms, int mk) {
+#define MXK(A, B) (const void*)mx::taylor_mx_kernel<NPT, NCH, A, B>
+  if (ms == 1) return mk == 1 ? MXK(1, 1) : MXK(1, 2);
+  if (ms == 2) return mk == 2 ? MXK(2, 2) : MXK(2, 3);
+  if (ms == 3) return mk == 3 ? MXK(3, 3) : MXK(3, 4);
+  return MXK(4, 4);
+#undef MXK
+}
+
+static const void* mx_fn(const Params& p) {
+  const mx::Geo g = mx::make_geo(p);
+  const int nch = mx::nch_for(g);
+  const int ms = mx::snf_m(g.W), mk = mx::snf_m(g.KW);
+  if (p.NP > 2) return nch == 16 ? mx_fn_ms<4, 16>(ms, mk) : nch == 8 ? mx_fn_ms<4, 8>(ms, mk) : mx_fn_ms<4, 4>(ms, mk);
+  return nch == 16 ? mx_fn_ms<2, 16>(ms, mk) : nch == 8 ? mx_fn_ms<2, 8>(ms, mk) : mx_fn_ms<2, 4>(ms, mk);
+}
+
+cudaError_t launch_mx_kernel(const Params& p, int G, size_t smem, cudaStream_t stream) {
+  const void* fn = mx_fn(p);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (G > 8) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.n_traj * G);
+  cfg.blockDim = dim3(mx::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  Params pc = p;
+  void* args[] = {&pc};
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+int mx_max_cluster(const Params& p, size_t smem, int want) {
+  const void* fn = mx_fn(p);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (want > 8) cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(want);
+  cfg.blockDim = dim3(mx::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = want;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+}  // namespace mpt

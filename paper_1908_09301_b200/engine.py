@@ -107,10 +107,29 @@ class DevicePlan:
         kern, cl = ctypes.c_int32(), ctypes.c_int32()
         _native.check(self.lib.mpt_plan_kernel(self.h, ctypes.byref(kern), ctypes.byref(cl)))
         return {"smem_bytes": s.value, "k_chunk": k.value, "threads": t.value,
-                "kernel": {1: "team", 2: "cluster", 3: "pipe", 4: "grid", 5: "relay"}.get(kern.value, "?"), "cluster": cl.value}
+                "kernel": {1: "team", 2: "cluster", 3: "pipe", 4: "grid", 5: "relay", 6: "mx"}.get(kern.value, "?"), "cluster": cl.value}
+
+    @property
+    def variant(self) -> int:
+        """Arithmetic variant of the selected kernel (oracle/fixmodel.c): 1 for the
+        matrix-recurrence kernel, 0 for the per-order C-product kernels."""
+        kern, cl = ctypes.c_int32(), ctypes.c_int32()
+        _native.check(self.lib.mpt_plan_kernel(self.h, ctypes.byref(kern), ctypes.byref(cl)))
+        return 1 if kern.value == 6 else 0
+
+    def model_kwargs(self) -> dict:
+        """Arguments that make oracle/fixmodel.c reproduce this plan's kernel bit for
+        bit (test infrastructure): the arithmetic variant and, for the matrix
+        recurrence, the number of bulk CTAs (their partition of the Cauchy sums
+        enters the rounding)."""
+        kern, cl = ctypes.c_int32(), ctypes.c_int32()
+        _native.check(self.lib.mpt_plan_kernel(self.h, ctypes.byref(kern), ctypes.byref(cl)))
+        if kern.value == 6:
+            return {"variant": 1, "bulk": cl.value - 1}
+        return {"variant": 0}
 
     def configure(self, kernel: str = "auto", cluster: int = 8):
-        code = {"auto": 0, "team": 1, "cluster": 2, "pipe": 3, "grid": 4, "relay": 5}[kernel]
+        code = {"auto": 0, "team": 1, "cluster": 2, "pipe": 3, "grid": 4, "relay": 5, "mx": 6}[kernel]
         _native.check(self.lib.mpt_plan_configure(self.h, code, cluster))
 
     def _state(self, state: np.ndarray) -> np.ndarray:

@@ -43,7 +43,8 @@ def test_integrate_bit_exact_vs_model(gpu, P, N, steps, stride):
     st = fmt.to_digits([M.mp_from_decimal(t, ctx) for t in CANON_INIT])
     with DevicePlan(tables, fmt, N, 1) as plan:
         s_gpu, r_gpu, status = plan.integrate(st, steps, 0, stride)
-    s_cpu, r_cpu = FX.integrate(tables, fmt.frac_digits, N, P, st, steps, 0, stride)
+        kw = plan.model_kwargs()
+    s_cpu, r_cpu = FX.integrate(tables, fmt.frac_digits, N, P, st, steps, 0, stride, **kw)
     assert status.tolist() == [0]
     assert list(s_gpu) == list(s_cpu)
     assert np.array_equal(r_gpu[:, 0], r_cpu)
@@ -52,7 +53,7 @@ def test_integrate_bit_exact_vs_model(gpu, P, N, steps, stride):
 @pytest.mark.parametrize("kernel,cluster", [("team", 1), ("cluster", 1), ("cluster", 2), ("cluster", 8),
                                             ("cluster", 16), ("pipe", 1), ("pipe", 2), ("pipe", 4), ("pipe", 16),
                                             ("relay", 2), ("relay", 3), ("relay", 8), ("relay", 16),
-                                            ("grid", 1)])
+                                            ("grid", 1), ("mx", 2), ("mx", 3), ("mx", 5), ("mx", 8), ("mx", 16)])
 @pytest.mark.parametrize("P,N,steps", [(167, 40, 12), (1661, 200, 2)])
 def test_every_kernel_bit_exact_vs_model(gpu, kernel, cluster, P, N, steps):
     ctx, system, fmt, tables = lorenz_tables(P, N)
@@ -66,7 +67,8 @@ def test_every_kernel_bit_exact_vs_model(gpu, kernel, cluster, P, N, steps):
         info = plan.info()
         assert info["kernel"] == kernel
         s_gpu, r_gpu, status = plan.integrate(st, steps, 0, 1)
-    s_cpu, r_cpu = FX.integrate(tables, fmt.frac_digits, N, P, st, steps, 0, 1)
+        kw = plan.model_kwargs()
+    s_cpu, r_cpu = FX.integrate(tables, fmt.frac_digits, N, P, st, steps, 0, 1, **kw)
     assert np.array_equal(r_gpu[:, 0], r_cpu), info
 
 
@@ -91,7 +93,8 @@ def test_jet_bit_exact_vs_model_large_order(gpu):
     st = fmt.to_digits([M.mp_from_decimal(t, ctx) for t in CANON_INIT])
     with DevicePlan(tables, fmt, N, 1) as plan:
         g = plan.compute_jet(st)[0]
-    c = FX.compute_jet(tables, fmt.frac_digits, N, st)
+        kw = plan.model_kwargs()
+    c = FX.compute_jet(tables, fmt.frac_digits, N, st, **kw)
     assert np.array_equal(g, c)
 
 
@@ -102,9 +105,10 @@ def test_ensemble_of_trajectories_bit_exact(gpu):
     states = np.stack([fmt.to_digits([b + Fraction(j, 10**20) for b in base]) for j in range(n_traj)])
     with DevicePlan(tables, fmt, N, n_traj) as plan:
         _, r_gpu, status = plan.integrate(states, 12, 0, 4)
+        kw = plan.model_kwargs()
     assert not status.any()
     for j in range(n_traj):
-        _, r_cpu = FX.integrate(tables, fmt.frac_digits, N, P, states[j], 12, 0, 4)
+        _, r_cpu = FX.integrate(tables, fmt.frac_digits, N, P, states[j], 12, 0, 4, **kw)
         assert np.array_equal(r_gpu[:, j], r_cpu), j
 
 
@@ -120,7 +124,8 @@ def test_random_quadratic_systems_jets_bit_exact(golden, gpu):
         st = fmt.to_digits([frac(h) for h in c["state"]])
         with DevicePlan(tables, fmt, N, 1) as plan:
             g = plan.compute_jet(st)[0]
-        assert np.array_equal(g, FX.compute_jet(tables, fmt.frac_digits, N, st)), name
+            kw = plan.model_kwargs()
+        assert np.array_equal(g, FX.compute_jet(tables, fmt.frac_digits, N, st, **kw)), name
 
 
 # ---------------------------------------------------- parity vs reference

@@ -1,6 +1,6 @@
 import sys, os, ctypes, numpy as np
 os.environ['MPT_DEBUG']='1'
-sys.path.insert(0,'.')
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1908_09301_b200 as M
 from paper_1908_09301_b200.engine import SystemTables, DevicePlan
 from paper_1908_09301_b200.fixed import FixedFormat
