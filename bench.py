@@ -229,6 +229,7 @@ def run_b200(args, rank, world, local_rank):
     _native.check(lib.mpt_imad_probe(device, ctypes.byref(peak), ctypes.byref(pms)))
 
     plan = DevicePlan(w["tables"], w["fmt"], w["N"], w["n_local"], device)
+    kinfo = plan.info()
     plan.upload(w["states"])
     # warm-up; the last warm-up launch counts limb-MACs for the roofline
     for k in range(args.warmup):
@@ -319,6 +320,7 @@ def run_b200(args, rank, world, local_rank):
                        "frac_bits": w["fmt"].frac_bits, "tau": w["tau_text"], "taylor_steps_per_bench_step": S,
                        "trajectories_total": w["n_total"], "trajectories_per_gpu": w["n_local"],
                        "l2": "flushed between timed launches (256 MiB memset, outside the kernel events)",
+                       "kernel": kinfo["kernel"], "cluster_ctas": kinfo["cluster"],
                        "parallelism": (f"ensemble sharded over {world} GPUs" if w["strong"]
                                        else f"one trajectory per GPU ({world} replicas, weak)")},
             "roofline": {"bound": "int", "achieved": achieved, "peak": peak.value, "unit": "limb-MAC/s",

@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(256, 1) taylor_team_kernel(const __grid_consta
 
 // Integer-pipe roofline probe: every thread runs 8 independent IMAD.WIDE
 // chains (s64 += s32 * s32) -- the instruction the Cauchy loop is built on.
-__global__ void imad_wide_probe(int iters, int32_t seed, long long* out) {
+__global__ void __launch_bounds__(512) imad_wide_probe(int iters, int32_t seed, long long* out) {
   int64_t acc[8];
 #pragma unroll
   for (int c = 0; c < 8; c++) acc[c] = seed + c;
@@ -455,7 +455,11 @@ __global__ void imad_wide_probe(int iters, int32_t seed, long long* out) {
 #pragma unroll
     for (int u = 0; u < 8; u++) {
 #pragma unroll
-      for (int c = 0; c < 8; c++) acc[c] = mad_wide(x + c, y, acc[c]);
+      for (int c = 0; c < 8; c++) {
+        int64_t d;  // one fused IMAD.WIDE (s64 += s32 * s32), as in the kernels' inner loops
+        asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(d) : "r"(x + c), "r"(y), "l"(acc[c]));
+        acc[c] = d;
+      }
       y += u;
     }
   }

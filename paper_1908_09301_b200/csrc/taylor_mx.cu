@@ -91,7 +91,7 @@ __host__ __device__ inline int n_entries(const Params& p, int* em, int* ej, int*
 
 struct Layout {
   int Gb, nE, nslots;
-  size_t off_lrow, off_linfo, off_cpart, off_lsum, off_cbuf, off_recv, off_ssum, lead_total;
+  size_t off_lrow, off_linfo, off_cpart, off_lsum, off_cbuf, off_recv, off_ssum, off_cinf, lead_total;
   size_t off_rows, off_rinfo, off_srow, off_sinfo, off_crow, off_cinfo, off_wcol, off_acc, off_bcc, off_kst,
       off_kcol, bulk_total;
   size_t total;
@@ -136,6 +136,7 @@ __host__ __device__ inline Layout make_layout(const Params& p, int G) {
   L.off_cbuf = take(sizeof(int64_t) * (size_t)2 * kMaxD * g.ncp);
   L.off_recv = take(sizeof(int64_t) * 2 * (size_t)(L.Gb > 0 ? L.Gb : 1) * NPp * g.ncp);
   L.off_ssum = take(sizeof(int64_t) * (size_t)p.D * (g.W + 3));
+  L.off_cinf = take(sizeof(int2) * (size_t)p.N);
   L.lead_total = o;
   o = 0;
   L.nslots = row_slots(p, G, -1, nullptr);
@@ -187,6 +188,16 @@ __device__ __forceinline__ void bulk_push(uint32_t rdst, uint32_t lsrc, uint32_t
   asm volatile(
       "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(rdst),
       "r"(lsrc), "r"(bytes), "r"(rbar)
+      : "memory");
+}
+// one TMA bulk copy from global memory into the same shared offset of every CTA
+// in `mask` (cluster ranks), completing `bytes` on each one's mbarrier (same offset)
+__device__ __forceinline__ void bulk_multicast(uint32_t ldst, const void* gsrc, uint32_t bytes, uint32_t lbar,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(
+          ldst),
+      "l"(gsrc), "r"(bytes), "r"(lbar), "h"(mask)
       : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
@@ -338,6 +349,46 @@ __device__ __forceinline__ void sts64(uint32_t a, int64_t v) {
   asm volatile("st.shared.b64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
 }
 
+// one masked chunk of 4 p-steps: acc[r] += sum_{p in [p0, min(p0+3, p1)]} A[p] B[c0+r-p]
+__device__ __forceinline__ void mac_chunk4(int64_t (&acc)[8], uint32_t A, uint32_t B, int c0, int p0, int p1) {
+  int32_t a[4], b[11];
+#pragma unroll
+  for (int u = 0; u < 4; u++) a[u] = (p0 + u <= p1) ? lds32(A + 4 * (p0 + u)) : 0;
+#pragma unroll
+  for (int t = 0; t < 11; t++) b[t] = lds32(B + 4 * (c0 - p0 - 3 + t));  // b[t] = B[c0 - p0 - 3 + t]
+#pragma unroll
+  for (int u = 0; u < 4; u++)
+#pragma unroll
+    for (int r = 0; r < 8; r++) acc[r] = madw(a[u], b[r - u + 3], acc[r]);
+}
+
+// acc += sum_{p in [p0, p1]} A[p] B[c0+r-p]: one p-step per iteration (8
+// IMAD.WIDE on the 8-column window, no masked work), next operands loaded one
+// step ahead; rows are zero-padded, so the look-ahead reads are harmless
+__device__ __forceinline__ void mac_run(int64_t (&acc)[8], uint32_t A, uint32_t B, int c0, int p0, int p1) {
+#if MX_MAC_CHUNK4
+#pragma unroll 1
+  for (int q = p0; q <= p1; q += 4) mac_chunk4(acc, A, B, c0, q, p1);
+#else
+  if (p0 > p1) return;
+  int32_t w[8];
+#pragma unroll
+  for (int r = 0; r < 8; r++) w[r] = lds32(B + 4 * (c0 + r - p0));
+  int32_t a = lds32(A + 4 * p0), bn = lds32(B + 4 * (c0 - p0 - 1));
+#pragma unroll 2
+  for (int p = p0; p <= p1; p++) {
+    const int32_t an = lds32(A + 4 * (p + 1)), bnn = lds32(B + 4 * (c0 - p - 2));
+#pragma unroll
+    for (int r = 0; r < 8; r++) acc[r] = madw(a, w[r], acc[r]);
+#pragma unroll
+    for (int r = 7; r > 0; r--) w[r] = w[r - 1];
+    w[0] = bn;
+    a = an;
+    bn = bnn;
+  }
+#endif
+}
+
 // one masked block of 8 p-steps: acc[r] += sum_{p in [p0, min(p0+7, p1)]} A[p] B[c0+r-p];
 // straight-line code (8 loads of A, 15 of B, 64 IMAD.WIDE). Rows are zero-padded
 // by kPad digits, so the reads past the ranges are harmless.
@@ -394,29 +445,20 @@ __device__ __noinline__ void warp_prods(const Prod* desc, int nprod, int T, int 
     const Prod P = desc[k];
     if (gp >= npair || P.ia.y < 0 || P.ib.y < 0) continue;
     const int lo1 = max(P.ia.x, c01 - P.ib.y), hi1 = min(P.ia.y, c01 + 7 - P.ib.x);
-    const int nb1 = hi1 >= lo1 ? (hi1 - lo1 + 8) / 8 : 0;
-    int lo2 = 0, hi2 = -1, nb2 = 0;
+    int lo2 = 0, hi2 = -1;
     if (g2 > g1) {
       lo2 = max(P.ia.x, c02 - P.ib.y);
       hi2 = min(P.ia.y, c02 + 7 - P.ib.x);
-      nb2 = hi2 >= lo2 ? (hi2 - lo2 + 8) / 8 : 0;
     }
-#pragma unroll 1
-    for (int b = ch; b < nb1 + nb2; b += NCH) {
-      int64_t t[8];
-      const bool first = b < nb1;
-#pragma unroll
-      for (int r = 0; r < 8; r++) t[r] = 0;
-      mac_block(t, P.A, P.B, first ? c01 : c02, first ? lo1 + 8 * b : lo2 + 8 * (b - nb1), first ? hi1 : hi2);
-#pragma unroll
-      for (int r = 0; r < 8; r++) {
-        a1[r] += first ? t[r] : 0;
-        a2[r] += first ? 0 : t[r];
-      }
-    }
+    // this lane's share of the pair's concatenated p-ranges: [s0, s1)
+    const int len1 = hi1 >= lo1 ? hi1 - lo1 + 1 : 0, len2 = hi2 >= lo2 ? hi2 - lo2 + 1 : 0;
+    const int tot = len1 + len2;
+    const int s0 = (ch * tot) / NCH, s1 = ((ch + 1) * tot) / NCH;
+    mac_run(a1, P.A, P.B, c01, lo1 + s0, lo1 + min(s1, len1) - 1);
+    mac_run(a2, P.A, P.B, c02, lo2 + max(s0 - len1, 0), lo2 + s1 - len1 - 1);
     if (mc && ch == 0) {
       mc->useful += group_macs(P.ia, P.ib, c01) + (g2 > g1 ? group_macs(P.ia, P.ib, c02) : 0);
-      mc->executed += 64ull * (nb1 + nb2);
+      mc->executed += 8ull * tot;
     }
   }
   if (!accumulate)
@@ -496,6 +538,9 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
   __shared__ int s_em[kMaxD * kMaxD], s_ej[kMaxD * kMaxD], s_dyn[kMaxD * kMaxD];
   __shared__ int s_base[kMaxD], s_full[kMaxD];
   __shared__ Prod s_prod[kWarps][kPerWarpPass];
+  __shared__ int4 s_pl[4][kMaxProd];        // lead product lists: (kind, index, side, multiplier)
+  __shared__ int s_tr[4][2 * kMaxD + 1];    // per target: first product of the list
+  int2* s_cinfo = nullptr;                  // lead: nonzero range of C_i, every order
   __shared__ int s_wq[kWarps];
   cg::cluster_group cluster = cg::this_cluster();
   const int G = (int)cluster.num_blocks();
@@ -561,19 +606,65 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
       const int2 inf = row_info(LR(r), p.W);
       if (lane == 0) linfo[r] = inf;
     }
+    // product lists per order kind (0: j = 1, 1: j = 2, 2: 3 <= j <= N-1, 3: last order, rows only),
+    // grouped by target (U_j^0..D-1, then rows 0..D-1), and the C_i nonzero ranges
+    if (tid == 0) {
+      for (int lk = 0; lk < 4; lk++) {
+        const bool doU = lk != 3;
+        const int lagn = lk < 3 ? lk : 0;
+        int cnt = 0;
+        for (int tg = 0; tg < 2 * p.D; tg++) {
+          s_tr[lk][tg] = cnt;
+          if (tg < p.D && doU) {
+            for (int e = 0; e < nE; e++)
+              if (s_em[e] == tg) s_pl[lk][cnt++] = make_int4(0, e, 0, 1);
+            for (int t = 0; t < p.NT; t++)
+              if (p.teq[t] == tg)
+                for (int side = 0; side < lagn; side++) s_pl[lk][cnt++] = make_int4(2, t, side, p.tq_int[t]);
+          } else if (tg >= p.D) {
+            s_pl[lk][cnt++] = make_int4(1, tg - p.D, 0, 1);
+          }
+        }
+        s_tr[lk][2 * p.D] = cnt;
+      }
+    }
+    s_cinfo = (int2*)(smem + L.off_cinf);
+    for (int i = warp; i < N; i += kWarps) {
+      int bot = 1 << 30, tp = -1;
+      for (int d = lane; d < p.W; d += 32)
+        if (p.ctab[(size_t)i * p.RS + d]) {
+          bot = min(bot, d);
+          tp = max(tp, d);
+        }
+      bot = __reduce_min_sync(0xffffffffu, bot);
+      tp = __reduce_max_sync(0xffffffffu, tp);
+      if (lane == 0) s_cinfo[i] = make_int2(tp >= 0 ? bot : p.W, tp);
+    }
     __syncthreads();
     uint32_t rph = 0;
 
-    // lane 0 of a row warp: push new row m (index r, lead buffer `src`) to the bulk CTAs that keep it
+    // warp-wide: publish new row m (index r) through the global coefficient table:
+    // one TMA multicast into every bulk CTA for left-hand variables, one copy to
+    // the owner of r otherwise
+    int32_t* gcoef = p.coef + (size_t)traj * p.D * (N + 1) * p.RS;
     auto push_row = [&](int m, int r, const int32_t* src) {
-      const int sl = SLOT(m, r);
-      const uint32_t rb_local = bar_local + 8 * (r & 3);
-      fence_async_smem();
-      for (int dst = 1; dst < G; dst++) {
-        if (!s_full[m] && dst != owner(r)) continue;
-        bulk_push(mapa_u32(rows_remote + 4 * sl * g.rs, dst), smem_u32(src), (uint32_t)(g.urs * 4), mapa_u32(rb_local, dst));
+      int32_t* gdst = gcoef + ((size_t)m * (N + 1) + r) * p.RS;
+      for (int d = lane; d < p.RS; d += 32) gdst[d] = d < p.W ? src[d] : 0;
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        const int sl = SLOT(m, r);
+        const uint32_t rb_local = bar_local + 8 * (r & 3);
+        if (s_full[m]) {
+          bulk_multicast(rows_remote + 4 * sl * g.rs, gdst, (uint32_t)(g.urs * 4), rb_local,
+                         (uint16_t)(((1u << G) - 1u) & ~1u));
+        } else {
+          const int dst = owner(r);
+          bulk_push(mapa_u32(rows_remote + 4 * sl * g.rs, dst), smem_u32(src), (uint32_t)(g.urs * 4),
+                    mapa_u32(rb_local, dst));
+          bulk_commit();
+        }
       }
-      bulk_commit();
     };
     // C_i into buffer b (cp.async, 16-byte chunks; ctab rows are RS-strided, RS >= W, multiple of 4)
     auto prefetch_c = [&](int i, int b) {
@@ -659,11 +750,6 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
       asm volatile("cp.async.commit_group;" ::: "memory");
       asm volatile("cp.async.wait_all;" ::: "memory");
       __syncthreads();
-      if (warp == 0) {
-        const int2 inf = row_info(LR(R_C + 0), p.W);
-        if (lane == 0) linfo[R_C + 0] = inf;
-      }
-      __syncthreads();
 
       for (int i = 0; i < N; i++) {
         const int par = i & 1, j = i + 1;
@@ -673,8 +759,8 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
         LT(0);
         const bool doU = j <= N - 1;
         const int lagn = (j >= 2 && j <= N - 1) ? (j == 2 ? 1 : 2) : 0;
-        const int nEu = doU ? nE : 0;
-        const int P = nEu + p.D + p.NT * lagn;
+        const int lk = !doU ? 3 : lagn;  // product list of this order
+        const int P = s_tr[lk][2 * p.D];
         // prefetch C_{i+1}, K_{i+1} (their buffers were last read at order i-1)
         if (i + 1 < N) prefetch_c(i + 1, par ^ 1);
         if (i + 2 < N) prefetch_k(i + 1, par ^ 1);
@@ -682,25 +768,26 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
         if (warp < kMacWarps) {
 #pragma unroll 1
           for (int pi = warp; pi < P; pi += kMacWarps) {
+            const int4 d = s_pl[lk][pi];  // kind, index, side, -
             const int32_t *A, *B;
             int2 ia, ib;
             int T = g.Tc;
-            if (pi < nEu) {
-              A = LR(R_U + par * p.D + s_ej[pi]);
-              ia = linfo[R_U + par * p.D + s_ej[pi]];
-              B = LR(R_K + par * nE + pi);
-              ib = linfo[R_K + par * nE + pi];
-            } else if (pi < nEu + p.D) {
-              const int m = pi - nEu;
-              A = LR(R_U + par * p.D + m);
-              ia = linfo[R_U + par * p.D + m];
+            if (d.x == 0) {  // K entry
+              const int e = d.y, ru = R_U + par * p.D + s_ej[e];
+              A = LR(ru);
+              ia = linfo[ru];
+              B = LR(R_K + par * nE + e);
+              ib = linfo[R_K + par * nE + e];
+            } else if (d.x == 1) {  // new row
+              const int ru = R_U + par * p.D + d.y;
+              A = LR(ru);
+              ia = linfo[ru];
               B = LR(R_C + par);
-              ib = linfo[R_C + par];
-            } else {
-              const int l = pi - nEu - p.D, t = l / lagn, side = l - t * lagn;
-              const int a = p.pj[p.tpair[t]], b = p.pk[p.tpair[t]];
-              const int ra = (lagn == 2 && side == 0) ? R_ROW + par * p.D + a : R_ROW1 + a;
-              const int rb = (lagn == 2 && side == 1) ? R_ROW + par * p.D + b : R_ROW1 + b;
+              ib = s_cinfo[i];
+            } else {  // lag-1 term of bilinear term t = d.y (rows j-1 and 1)
+              const int t = d.y, a = p.pj[p.tpair[t]], b = p.pk[p.tpair[t]];
+              const int ra = (lagn == 2 && d.z == 1) ? R_ROW1 + a : R_ROW + par * p.D + a;
+              const int rb = (lagn == 2 && d.z == 0) ? R_ROW1 + b : R_ROW + par * p.D + b;
               A = LR(ra);
               ia = linfo[ra];
               B = LR(rb);
@@ -710,7 +797,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
             warp_product<NCH>(s_prod[warp], A, ia, B, ib, T, g, cpart + (size_t)pi * g.ncp, mc);
           }
         } else {
-          // aux warp: q_t * sum of the bulk CTAs' L'(j) into lsum[m]
+          // aux warp: q_t * sum of the bulk CTAs' L'(j) into lsum[m] (two columns per lane and load)
           const bool have = doU && j >= 4 && p.NP > 0;
           if (have) {
             const int rp = j & 1;
@@ -720,64 +807,55 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
           }
           const int64_t* rv = recv + (size_t)(j & 1) * Gb * NPp * g.ncp;
           for (int m = 0; m < p.D; m++)
-            for (int c = lane; c < g.ncols; c += 32) {
-              int64_t s = 0;
+            for (int c = 2 * lane; c < g.ncp; c += 64) {
+              longlong2 sacc = make_longlong2(0, 0);
               if (have)
                 for (int t = 0; t < p.NT; t++) {
                   if (p.teq[t] != m) continue;
                   const int q = p.tpair[t];
-                  int64_t v = 0;
-                  for (int r = 0; r < Gb; r++) v += rv[((size_t)r * NPp + q) * g.ncp + c];
-                  s += (int64_t)p.tq_int[t] * v;
+                  longlong2 v = make_longlong2(0, 0);
+#pragma unroll 4
+                  for (int r = 0; r < Gb; r++) {
+                    const longlong2 x = *(const longlong2*)(rv + ((size_t)r * NPp + q) * g.ncp + c);
+                    v.x += x.x;
+                    v.y += x.y;
+                  }
+                  sacc.x += (int64_t)p.tq_int[t] * v.x;
+                  sacc.y += (int64_t)p.tq_int[t] * v.y;
                 }
-              lsum[(size_t)m * g.ncp + c] = s;
+              *(longlong2*)(lsum + (size_t)m * g.ncp + c) = sacc;
             }
         }
         LT(1);
         __syncthreads();
         LT(2);
-        // ---- roundings: U_{j}^m (warps 0..D-1), rows a~_{i+1}^m (warps D..2D-1)
+        // ---- roundings: U_j^m (warps 0..D-1), rows a~_{i+1}^m (warps D..2D-1)
         if (warp < 2 * p.D) {
-          const bool isU = warp < p.D;
-          const int m = isU ? warp : warp - p.D;
+          const int tg = warp;
+          const bool isU = tg < p.D;
+          const int m = isU ? tg : tg - p.D;
           if (!isU || doU) {
-            int64_t* cv = cbuf + (size_t)warp * g.ncp;
+            int64_t* cv = cbuf + (size_t)tg * g.ncp;
+            const int k0 = s_tr[lk][tg], k1 = s_tr[lk][tg + 1];
             for (int c = lane; c < g.ncols; c += 32) {
-              int64_t s;
-              if (isU) {
-                s = lsum[(size_t)m * g.ncp + c];
-                for (int e = 0; e < nE; e++)
-                  if (s_em[e] == m) s += cpart[(size_t)e * g.ncp + c];
-                for (int l = 0; l < p.NT * lagn; l++) {
-                  const int t = l / lagn;
-                  if (p.teq[t] == m) s += (int64_t)p.tq_int[t] * cpart[(size_t)(nEu + p.D + l) * g.ncp + c];
-                }
-              } else {
-                s = cpart[(size_t)(nEu + m) * g.ncp + c];
-              }
-              cv[c] = s;
+              int64_t sacc = isU ? lsum[(size_t)m * g.ncp + c] : 0;
+#pragma unroll 4
+              for (int k = k0; k < k1; k++) sacc += (int64_t)s_pl[lk][k].w * cpart[(size_t)k * g.ncp + c];
+              cv[c] = sacc;
             }
             __syncwarp();
-            if (isU) {
-              if (warp_snf_call<MS>(cv, g.ncols, p.W, LR(R_U + (par ^ 1) * p.D + m), &linfo[R_U + (par ^ 1) * p.D + m]) &&
-                  lane == 0)
-                atomicOr(&s_flag, 1);
-            } else {
-              const int rr = R_ROW + (par ^ 1) * p.D + m;
-              if (lane == 0) bulk_wait_read();  // the copies of row i-1 (same buffer) have read it
+            const int rr = isU ? R_U + (par ^ 1) * p.D + m : R_ROW + (par ^ 1) * p.D + m;
+            if (!isU && lane == 0) bulk_wait_read();  // the owner copy of row i-1 (same buffer) has read it
+            __syncwarp();
+            if (warp_snf_call<MS>(cv, g.ncols, p.W, LR(rr), &linfo[rr]) && lane == 0) atomicOr(&s_flag, 1);
+            if (!isU) {  // row a~_j: publish, state sum, keep row 1
               __syncwarp();
-              if (warp_snf_call<MS>(cv, g.ncols, p.W, LR(rr), &linfo[rr]) && lane == 0) atomicOr(&s_flag, 1);
-              __syncwarp();
+              push_row(m, j, LR(rr));
               for (int d = lane; d < p.W; d += 32) ssum[(size_t)m * (p.W + 3) + d] += LR(rr)[d];
               if (i == 0) {
                 for (int d = lane; d < p.W; d += 32) LR(R_ROW1 + m)[d] = LR(rr)[d];
                 if (lane == 0) linfo[R_ROW1 + m] = linfo[rr];
               }
-              if (p.write_coef)
-                for (int d = lane; d < p.W; d += 32)
-                  p.coef[(((size_t)traj * p.D + m) * (N + 1) + j) * p.RS + d] = LR(rr)[d];
-              __syncwarp();
-              if (lane == 0) push_row(m, j, LR(rr));
             }
           }
         }
@@ -786,14 +864,10 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
         LT(4);
         __syncthreads();
         LT(5);
-        if (i + 1 < N && warp == 0) {
-          const int2 inf = row_info(LR(R_C + (par ^ 1)), p.W);
-          if (lane == 0) linfo[R_C + (par ^ 1)] = inf;
-        }
-        __syncthreads();
-        LT(6);
 #undef LT
       }
+      if (lane == 0) bulk_wait_read();
+      __syncthreads();
       // ---- end of step: state = RN_P(sum of rows)
       if (warp < p.D) {
         const int m = warp;
