@@ -44,6 +44,9 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kMacWarps = kWarps - 1;  // warp 15 of the lead gathers L'
 constexpr int kMaxProd = 32;           // products per lead stage
 constexpr int kPerWarpPass = 4;        // bulk products accumulated per lane before a split
+constexpr int kQ = 16;                 // zero-skipping width quantum (digits)
+constexpr int kMaxQ = 4;               // widths up to 64 digits (K <= ~500): 2 x 4 x 4 product shapes
+constexpr int kShapes = 2 * kMaxQ * kMaxQ;
 
 struct Geo {
   int W, KW, T, Tc, ncols, ncp, ng, rs, krs, urs;
@@ -91,9 +94,10 @@ __host__ __device__ inline int n_entries(const Params& p, int* em, int* ej, int*
 
 struct Layout {
   int Gb, nE, nslots;
-  size_t off_lrow, off_linfo, off_cpart, off_lsum, off_cbuf, off_recv, off_ssum, off_cinf, lead_total;
+  size_t off_lrow, off_linfo, off_cpart, off_lsum, off_cbuf, off_recv, off_ssum, off_cinf, off_scr, off_lshr, off_lshg,
+      lead_total;
   size_t off_rows, off_rinfo, off_srow, off_sinfo, off_crow, off_cinfo, off_wcol, off_acc, off_bcc, off_kst,
-      off_kcol, bulk_total;
+      off_kcol, off_bscr, off_bshr, off_bshg, bulk_total;
   size_t total;
 };
 
@@ -129,7 +133,7 @@ __host__ __device__ inline Layout make_layout(const Params& p, int G) {
     return r;
   };
   const int nlrow = 2 * p.D + p.D * p.D + 2 * p.D + 2 * L.nE + 2 + 3 * p.D;
-  L.off_lrow = take(sizeof(int32_t) * ((size_t)nlrow * g.rs + 2 * kPad));
+  L.off_lrow = take(sizeof(int32_t) * ((size_t)nlrow * g.rs + 3 * kPad));
   L.off_linfo = take(sizeof(int2) * (size_t)nlrow);
   L.off_cpart = take(sizeof(int64_t) * (size_t)kMaxProd * g.ncp);
   L.off_lsum = take(sizeof(int64_t) * (size_t)kMaxD * g.ncp);
@@ -137,10 +141,13 @@ __host__ __device__ inline Layout make_layout(const Params& p, int G) {
   L.off_recv = take(sizeof(int64_t) * 2 * (size_t)(L.Gb > 0 ? L.Gb : 1) * NPp * g.ncp);
   L.off_ssum = take(sizeof(int64_t) * (size_t)p.D * (g.W + 3));
   L.off_cinf = take(sizeof(int2) * (size_t)p.N);
+  L.off_scr = take(sizeof(int64_t) * (size_t)kWarps * 32 * 8);
+  L.off_lshr = take(0);
+  L.off_lshg = take(0);
   L.lead_total = o;
   o = 0;
   L.nslots = row_slots(p, G, -1, nullptr);
-  L.off_rows = take(sizeof(int32_t) * ((size_t)L.nslots * g.rs + 2 * kPad));
+  L.off_rows = take(sizeof(int32_t) * ((size_t)L.nslots * g.rs + 3 * kPad));
   L.off_rinfo = take(sizeof(int2) * (size_t)L.nslots);
   L.off_srow = take(sizeof(int32_t) * ((size_t)p.D * p.D * g.rs + 2 * kPad));
   L.off_sinfo = take(sizeof(int2) * (size_t)p.D * p.D);
@@ -151,6 +158,9 @@ __host__ __device__ inline Layout make_layout(const Params& p, int G) {
   L.off_bcc = take(sizeof(int64_t) * (size_t)NPp * g.ncp);
   L.off_kst = take(sizeof(int32_t) * (size_t)kWarps * g.krs);
   L.off_kcol = take(sizeof(int64_t) * (size_t)kWarps * g.ncp);
+  L.off_bscr = take(sizeof(int64_t) * (size_t)kWarps * 32 * 8);
+  L.off_bshr = take(0);
+  L.off_bshg = take(0);
   L.bulk_total = o;
   L.total = L.lead_total > L.bulk_total ? L.lead_total : L.bulk_total;
   return L;
@@ -502,6 +512,271 @@ __device__ __noinline__ void warp_prods(const Prod* desc, int nprod, int T, int 
   __syncwarp();
 }
 
+// Several products per warp: lane l works on product l / LPP (LPP = NP2 * 2
+// lanes per product, NP2 = group pairs rounded up to a power of two), on group
+// pair gp and one half of the pair's p-range; the two halves of a pair are
+// reduced with one shuffle round and the exact columns of product k are
+// written to out + k * ostride (bytes). Longer per-lane runs (~len/2 p-steps)
+// amortise the setup and reduction that dominate short runs.
+template <int NP2>
+__device__ __noinline__ void warp_multi(const Prod* desc, int nprod, int T, int ng, uint32_t out, int ostride,
+                                        int ncp, int nout, MacCount* mc) {
+  constexpr int LPP = 2 * NP2;
+  const int lane = threadIdx.x & 31;
+  const int k = lane / LPP, gp = (lane % LPP) >> 1, ch = lane & 1;
+  const int npair = (ng + 1) / 2;
+  const bool act = k < nprod && gp < npair;
+  const int g1 = gp, g2 = ng - 1 - gp;
+  const int c01 = T + 8 * g1, c02 = T + 8 * g2;
+  int64_t a1[8], a2[8];
+#pragma unroll
+  for (int r = 0; r < 8; r++) a1[r] = a2[r] = 0;
+  const Prod P = desc[k < nprod ? k : 0];
+  if (act && P.ia.y >= 0 && P.ib.y >= 0) {
+    const int lo1 = max(P.ia.x, c01 - P.ib.y), hi1 = min(P.ia.y, c01 + 7 - P.ib.x);
+    int lo2 = 0, hi2 = -1;
+    if (g2 > g1) {
+      lo2 = max(P.ia.x, c02 - P.ib.y);
+      hi2 = min(P.ia.y, c02 + 7 - P.ib.x);
+    }
+    const int len1 = hi1 >= lo1 ? hi1 - lo1 + 1 : 0, len2 = hi2 >= lo2 ? hi2 - lo2 + 1 : 0;
+    const int tot = len1 + len2;
+    const int s0 = ch ? tot / 2 : 0, s1 = ch ? tot : tot / 2;
+    mac_run(a1, P.A, P.B, c01, lo1 + s0, lo1 + min(s1, len1) - 1);
+    mac_run(a2, P.A, P.B, c02, lo2 + max(s0 - len1, 0), lo2 + s1 - len1 - 1);
+    if (mc && ch == 0) {
+      mc->useful += group_macs(P.ia, P.ib, c01) + (g2 > g1 ? group_macs(P.ia, P.ib, c02) : 0);
+      mc->executed += 8ull * tot;
+    }
+  }
+  // zero-fill the rows of this warp's products, then one reduction round
+  for (int e = lane; e < nprod * ncp; e += 32) {
+    const int kk = e / ncp, c = e - kk * ncp;
+    sts64(out + kk * ostride + 8 * c, 0);
+  }
+  __syncwarp();
+  int64_t v[8];
+#pragma unroll
+  for (int r = 0; r < 8; r++) {
+    const int64_t send = ch ? a1[r] : a2[r];
+    const int64_t keep = ch ? a2[r] : a1[r];
+    v[r] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+  }
+  if (act) {
+    const int g = ch ? g2 : g1;
+    if (!(ch && g2 <= g1)) {
+#pragma unroll
+      for (int r = 0; r < 8; r++) {
+        const int rel = 8 * g + r;
+        if (rel < nout) sts64(out + k * ostride + 8 * rel, v[r]);
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// Branch-free lead products. For a product shape (truncation T, full-width
+// operands of W and Wb digits) the p-range of every 8-column group g is fixed:
+// [max(0, c0 - Wb + 1), min(W - 1, c0 + 7)], c0 = T + 8g. The 32 lanes of a
+// warp are dealt to the groups in proportion to their lengths, each lane
+// getting one run of <= kRun p-steps of one group (a table computed once per
+// kernel). A product is then: 8 + 7 + kRun loads, 8 x kRun IMAD.WIDE with
+// compile-time register indices, 8 partial columns to the warp's scratch,
+// and a segment sum per column. Zero digits beyond the operands' nonzero
+// ranges cost MACs but no branches.
+constexpr int kRun = 12;
+
+struct LaneRun {
+  int g, p0, ns;  // group, first p, steps (0 = idle)
+};
+
+__host__ __device__ inline int grp_len(int g, int T, int W, int Wb) {
+  const int c0 = T + 8 * g;
+  const int lo = c0 - Wb + 1 > 0 ? c0 - Wb + 1 : 0;
+  const int hi = c0 + 7 < W - 1 ? c0 + 7 : W - 1;
+  return hi >= lo ? hi - lo + 1 : 0;
+}
+
+// lanes per group (sum 32) for a shape; returns the largest run, or -1 if > kRun
+__device__ inline int plan_lanes(int T, int W, int Wb, int ng, int* nl) {
+  int tot = 0;
+  for (int g = 0; g < ng; g++) tot += grp_len(g, T, W, Wb);
+  int used = 0;
+  for (int g = 0; g < ng; g++) {
+    const int len = grp_len(g, T, W, Wb);
+    nl[g] = len > 0 ? max(1, (32 * len) / (tot > 0 ? tot : 1)) : 0;
+    used += nl[g];
+  }
+  while (used > 32) {  // take lanes from the group with the shortest resulting runs
+    int best = -1, bl = 1 << 30;
+    for (int g = 0; g < ng; g++)
+      if (nl[g] > 1) {
+        const int len = grp_len(g, T, W, Wb), r = (len + nl[g] - 2) / (nl[g] - 1);
+        if (r < bl) {
+          bl = r;
+          best = g;
+        }
+      }
+    if (best < 0) return -1;
+    nl[best]--;
+    used--;
+  }
+  while (used < 32) {  // give spare lanes to the group with the longest runs
+    int best = -1, bl = -1;
+    for (int g = 0; g < ng; g++) {
+      const int len = grp_len(g, T, W, Wb);
+      if (nl[g] == 0) continue;
+      const int r = (len + nl[g] - 1) / nl[g];
+      if (r > bl) {
+        bl = r;
+        best = g;
+      }
+    }
+    if (best < 0) break;
+    nl[best]++;
+    used++;
+  }
+  int mx = 0;
+  for (int g = 0; g < ng; g++)
+    if (nl[g]) mx = max(mx, (grp_len(g, T, W, Wb) + nl[g] - 1) / nl[g]);
+  return mx <= kRun ? mx : -1;
+}
+
+// this lane's run and the lane range of every group (gl[g] = first lane, gl[ng] = 32)
+__device__ inline LaneRun lane_run(int T, int W, int Wb, int ng, int lane, int* gl) {
+  int nl[32];
+  LaneRun lr{0, 0, 0};
+  if (plan_lanes(T, W, Wb, ng, nl) < 0) return lr;
+  int first = 0;
+  for (int g = 0; g < ng; g++) {
+    gl[g] = first;
+    const int len = grp_len(g, T, W, Wb);
+    if (lane >= first && lane < first + nl[g]) {
+      const int k = lane - first;
+      const int c0 = T + 8 * g;
+      const int lo = c0 - Wb + 1 > 0 ? c0 - Wb + 1 : 0;
+      const int s0 = (k * len) / nl[g], s1 = ((k + 1) * len) / nl[g];
+      lr = LaneRun{g, lo + s0, s1 - s0};
+    }
+    first += nl[g];
+  }
+  gl[ng] = first;
+  return lr;
+}
+
+// Zero-skipping: the schedule of a product whose operands' top nonzero digits
+// are a1, b1 is the one of the shape (T, Wa, Wb) with Wa, Wb the widths
+// rounded up to multiples of kQ (digits above a row's top are zero, so the
+// result is unchanged). Tables for every (truncation, Wa, Wb) are built once
+// per kernel in shared memory: run[shape][lane] and gl[shape][33].
+
+__host__ __device__ inline int shape_id(int tsel, int qa, int qb) { return (tsel * kMaxQ + qa - 1) * kMaxQ + qb - 1; }
+
+// top nonzero digit of a row (warp-wide; -1 if zero)
+__device__ __forceinline__ int row_top(const int32_t* A, int W) {
+  int t = -1;
+  for (int base = 0; base < W; base += 32) {
+    const int d = base + (threadIdx.x & 31);
+    const unsigned m = __ballot_sync(0xffffffffu, d < W && A[d] != 0);
+    if (m) t = base + 31 - __clz(m);
+  }
+  return t;
+}
+
+// this lane's share of A (x) B accumulated into acc (fixed schedule `lr`)
+__device__ __forceinline__ void run_acc(int64_t (&acc)[8], const int32_t* A, const int32_t* B, int T, LaneRun lr) {
+  {
+    const int c0 = T + 8 * lr.g;
+    int32_t a[kRun], b[kRun + 7];
+#pragma unroll
+    for (int u = 0; u < kRun; u++) a[u] = u < lr.ns ? A[lr.p0 + u] : 0;
+#pragma unroll
+    for (int t = 0; t < kRun + 7; t++) b[t] = B[c0 - lr.p0 - (kRun - 1) + t];  // b[t] = B[c0 - p0 - kRun + 1 + t]
+#pragma unroll
+    for (int u = 0; u < kRun; u++)
+#pragma unroll
+      for (int r = 0; r < 8; r++) acc[r] = madw(a[u], b[r - u + kRun - 1], acc[r]);
+  }
+}
+
+// the lanes' windows -> exact columns out[0..ncp) (segment sum per group; `gl` = lane table)
+__device__ __forceinline__ void run_reduce(const int64_t (&acc)[8], const int* gl, int ng, int64_t* scr, int64_t* out,
+                                           int nout, int ncp, bool accumulate = false) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int r = 0; r < 8; r++) scr[lane * 8 + r] = acc[r];
+  __syncwarp();
+  for (int c = lane; c < ncp; c += 32) {
+    int64_t s = 0;
+    if (c < nout && c < 8 * ng) {
+      const int g = c >> 3, r = c & 7;
+      for (int l = gl[g]; l < gl[g + 1]; l++) s += scr[l * 8 + r];
+    }
+    out[c] = accumulate ? out[c] + s : s;
+  }
+  __syncwarp();
+}
+
+// shape tables (shared): run[shape * 32 + lane] = (group, p0, steps, ok), gl[shape * 33 + g]
+__device__ inline void build_shapes(int T, int Tc, int W, int KW, int ng, int4* run, int* gl) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int sh = warp; sh < kShapes; sh += kThreads / 32) {
+    const int tsel = sh / (kMaxQ * kMaxQ), qa = (sh / kMaxQ) % kMaxQ + 1, qb = sh % kMaxQ + 1;
+    const int Tt = tsel ? Tc : T;
+    const int Wa = min(qa * kQ, W), Wb = min(qb * kQ, KW);
+    const int ngs = max(0, min(ng, (Wa + Wb - 2 - Tt) / 8 + 1));
+    int glt[33];
+    int nl[32];
+    const bool ok = ngs > 0 && plan_lanes(Tt, Wa, Wb, ngs, nl) >= 0;
+    LaneRun lr{0, 0, 0};
+    if (ok) lr = lane_run(Tt, Wa, Wb, ngs, lane, glt);
+    run[sh * 32 + lane] = make_int4(lr.g, lr.p0, lr.ns, ok ? ngs : 0);
+    if (lane == 0 && ok)
+      for (int g = 0; g <= ngs; g++) gl[sh * 33 + g] = glt[g];
+  }
+}
+
+// zero-skipping exact product on one warp: out (=|+=) A (x) B, truncation Tt (tsel),
+// A of Wa_full digits, B of Wb_full; falls back to the full-width schedule `lrf`/`glf`
+__device__ __forceinline__ void zs_product(const int32_t* A, int Wa_full, const int32_t* B, int Wb_full, int tsel,
+                                           int Tt, const int4* run, const int* glbase, LaneRun lrf, const int* glf,
+                                           int ngf, int64_t* scr, int64_t* out, int nout, int ncp, bool accumulate,
+                                           MacCount* mc) {
+  const int lane = threadIdx.x & 31;
+  const int a1 = row_top(A, Wa_full), b1 = row_top(B, Wb_full);
+  if (a1 < 0 || b1 < 0 || a1 + b1 < Tt) {
+    if (!accumulate)
+      for (int c = lane; c < ncp; c += 32) out[c] = 0;
+    __syncwarp();
+    return;
+  }
+  const int qa = min(a1 / kQ + 1, kMaxQ), qb = min(b1 / kQ + 1, kMaxQ);
+  const int sh = shape_id(tsel, qa, qb);
+  const int4 rr = run[sh * 32 + lane];
+  const bool ok = __shfl_sync(0xffffffffu, rr.w, 0) > 0;
+  const LaneRun lr = ok ? LaneRun{rr.x, rr.y, rr.z} : lrf;
+  const int* gl = ok ? glbase + sh * 33 : glf;
+  const int ng = ok ? rr.w : ngf;
+  int64_t acc[8];
+#pragma unroll
+  for (int r = 0; r < 8; r++) acc[r] = 0;
+  run_acc(acc, A, B, Tt, lr);
+  run_reduce(acc, gl, ng, scr, out, nout, ncp, accumulate);
+  if (mc) mc->executed += 8ull * lr.ns;
+}
+
+// exact columns of A (x) B (W- and Wb-digit rows, zero-padded) into out[0..nout):
+// `scr` = this warp's scratch (32 x 8 int64), `gl` = the shape's lane table
+__device__ __forceinline__ void lead_product(const int32_t* A, const int32_t* B, int T, LaneRun lr, const int* gl,
+                                             int ng, int64_t* scr, int64_t* out, int nout, int ncp) {
+  int64_t acc[8];
+#pragma unroll
+  for (int r = 0; r < 8; r++) acc[r] = 0;
+  run_acc(acc, A, B, T, lr);
+  run_reduce(acc, gl, ng, scr, out, nout, ncp);
+}
+
 __device__ __forceinline__ Prod mkprod(const int32_t* A, int2 ia, const int32_t* B, int2 ib) {
   return Prod{smem_u32(A), smem_u32(B), ia, ib};
 }
@@ -540,6 +815,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
   __shared__ Prod s_prod[kWarps][kPerWarpPass];
   __shared__ int4 s_pl[4][kMaxProd];        // lead product lists: (kind, index, side, multiplier)
   __shared__ int s_tr[4][2 * kMaxD + 1];    // per target: first product of the list
+  __shared__ int s_gl[3][33];               // lead: first lane of every group, per product shape
   int2* s_cinfo = nullptr;                  // lead: nonzero range of C_i, every order
   __shared__ int s_wq[kWarps];
   cg::cluster_group cluster = cg::this_cluster();
@@ -575,7 +851,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
   const int R_ST = 0, R_SB = p.D, R_LIN = 2 * p.D, R_U = R_LIN + p.D * p.D, R_K = R_U + 2 * p.D,
             R_C = R_K + 2 * nE, R_ROW = R_C + 2, R_ROW1 = R_ROW + 2 * p.D;
   if (rank == 0) {
-    int32_t* lrow = (int32_t*)(smem + L.off_lrow) + kPad;
+    int32_t* lrow = (int32_t*)(smem + L.off_lrow) + 2 * kPad;
     for (int r = 0; r < p.D * p.D; r++)
       for (int d = tid; d < p.W; d += kThreads) lrow[(size_t)(R_LIN + r) * g.rs + d] = p.lin[(size_t)r * p.RS + d];
     for (int m = 0; m < p.D; m++)
@@ -592,7 +868,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
 
   if (rank == 0) {
     // =============================== lead ===============================
-    int32_t* lrow = (int32_t*)(smem + L.off_lrow) + kPad;
+    int32_t* lrow = (int32_t*)(smem + L.off_lrow) + 2 * kPad;
     int2* linfo = (int2*)(smem + L.off_linfo);
     int64_t* cpart = (int64_t*)(smem + L.off_cpart);
     int64_t* lsum = (int64_t*)(smem + L.off_lsum);
@@ -600,7 +876,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
     int64_t* recv = (int64_t*)(smem + L.off_recv);
     int64_t* ssum = (int64_t*)(smem + L.off_ssum);
     auto LR = [&](int r) { return lrow + (size_t)r * g.rs; };
-    const uint32_t rows_remote = smem_u32(smem + L.off_rows) + 4 * kPad;
+    const uint32_t rows_remote = smem_u32(smem + L.off_rows) + 4 * 2 * kPad;
     for (int r = warp; r < R_U; r += kWarps) {
       if (r >= R_SB && r < R_LIN) continue;
       const int2 inf = row_info(LR(r), p.W);
@@ -628,6 +904,20 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
         s_tr[lk][2 * p.D] = cnt;
       }
     }
+    // branch-free product schedules: shapes 0 = U x K (Tc, W, W+1), 1 = U x C (Tc, W, W), 2 = row x row (T, W, W)
+    const LaneRun lr0 = lane_run(g.Tc, p.W, g.KW, g.ng, lane, s_gl[0]);
+    const LaneRun lr1 = lane_run(g.Tc, p.W, p.W, g.ng, lane, s_gl[1]);
+    const LaneRun lr2 = lane_run(g.T, p.W, p.W, g.ng, lane, s_gl[2]);
+    int nlt[32];
+    const bool fast = g.ng <= 32 && plan_lanes(g.Tc, p.W, g.KW, g.ng, nlt) >= 0 &&
+                      plan_lanes(g.Tc, p.W, p.W, g.ng, nlt) >= 0 && plan_lanes(g.T, p.W, p.W, g.ng, nlt) >= 0;
+    int64_t* scr = (int64_t*)(smem + L.off_scr) + (size_t)warp * 32 * 8;
+    int4* shr = (int4*)(smem + L.off_lshr);
+    int* shg = (int*)(smem + L.off_lshg);
+    // zero-skipping schedules (zs_product) measured slower at K=500: the per-product
+    // segment reduction costs more than the skipped MACs; off until the reduction is fused
+    constexpr bool zskip = false;
+    if (zskip) build_shapes(g.T, g.Tc, p.W, g.KW, g.ng, shr, shg);
     s_cinfo = (int2*)(smem + L.off_cinf);
     for (int i = warp; i < N; i += kWarps) {
       int bot = 1 << 30, tp = -1;
@@ -753,7 +1043,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
 
       for (int i = 0; i < N; i++) {
         const int par = i & 1, j = i + 1;
-        const bool tlog = p.dbg && n == p.start_step + 1 && i < 64 && lane == 0;
+        const bool tlog = p.dbg && n == p.start_step + 1 && i < 256 && lane == 0;
 #define LT(k) \
   if (tlog) p.dbg[((size_t)i * 16 + warp) * 8 + (k)] = (long long)clock64();
         LT(0);
@@ -794,7 +1084,20 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
               ib = linfo[rb];
               T = g.T;
             }
-            warp_product<NCH>(s_prod[warp], A, ia, B, ib, T, g, cpart + (size_t)pi * g.ncp, mc);
+            if (zskip) {
+              const LaneRun lr = d.x == 0 ? lr0 : (d.x == 1 ? lr1 : lr2);
+              zs_product(A, p.W, B, d.x == 0 ? g.KW : p.W, d.x == 2 ? 0 : 1, T, shr, shg, lr, s_gl[d.x], g.ng, scr,
+                         cpart + (size_t)pi * g.ncp, g.ncols, g.ncp, false, mc);
+            } else if (fast) {
+              const LaneRun lr = d.x == 0 ? lr0 : (d.x == 1 ? lr1 : lr2);
+              lead_product(A, B, T, lr, s_gl[d.x], g.ng, scr, cpart + (size_t)pi * g.ncp, g.ncols, g.ncp);
+              if (mc) {
+                if (lane == s_gl[d.x][lr.g]) mcount.useful += group_macs(ia, ib, T + 8 * lr.g);
+                mcount.executed += 8ull * lr.ns;
+              }
+            } else {
+              warp_product<NCH>(s_prod[warp], A, ia, B, ib, T, g, cpart + (size_t)pi * g.ncp, mc);
+            }
           }
         } else {
           // aux warp: q_t * sum of the bulk CTAs' L'(j) into lsum[m] (two columns per lane and load)
@@ -888,7 +1191,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
   } else {
     // =============================== bulk ===============================
     const int o = rank;
-    int32_t* rows = (int32_t*)(smem + L.off_rows) + kPad;
+    int32_t* rows = (int32_t*)(smem + L.off_rows) + 2 * kPad;
     int2* rinfo = (int2*)(smem + L.off_rinfo);
     int32_t* srow = (int32_t*)(smem + L.off_srow) + kPad;
     int2* sinfo = (int2*)(smem + L.off_sinfo);
@@ -902,25 +1205,47 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
     auto ROW = [&](int v, int k) { return rows + (size_t)SLOT(v, k) * g.rs; };
     auto RINF = [&](int v, int k) { return rinfo[SLOT(v, k)]; };
     const uint32_t recv_remote = smem_u32(smem + L.off_recv);
-    const int32_t* lead_state = cluster.map_shared_rank((int32_t*)(smem + L.off_lrow) + kPad, 0);
+    const int32_t* lead_state = cluster.map_shared_rank((int32_t*)(smem + L.off_lrow) + 2 * kPad, 0);
     uint32_t rph4 = 0;  // phase bits of the 4 row barriers
+    // branch-free schedule for row x row products (shape T, W, W)
+    const LaneRun lrb = lane_run(g.T, p.W, p.W, g.ng, lane, s_gl[2]);
+    int nlb[32];
+    const bool bfast = g.ng <= 32 && plan_lanes(g.T, p.W, p.W, g.ng, nlb) >= 0;
+    int64_t* bscr = (int64_t*)(smem + L.off_bscr) + (size_t)warp * 32 * 8;
+    int4* bshr = (int4*)(smem + L.off_bshr);
+    int* bshg = (int*)(smem + L.off_bshg);
+    constexpr bool bzskip = false;
+    if (bzskip) build_shapes(g.T, g.Tc, p.W, g.KW, g.ng, bshr, bshg);
+    __syncthreads();
     int nfull = 0;
     for (int v = 0; v < p.D; v++) nfull += s_full[v];
 
     // exact per-CTA accumulation: every warp's exact partial columns -> (A, B) = (sum of low digits, sum of carries)
     auto absorb = [&](int nw_used) {
       __syncthreads();
-      for (int e = tid; e < p.NP * g.ncols; e += kThreads) {
-        const int q = e / g.ncols, c = e - q * g.ncols;
-        int64_t a = 0, b = 0;
-        for (int w = 0; w < nw_used; w++)
-          if (s_wq[w] == q) {
-            const int64_t v = wcol[(size_t)w * g.ncp + c];
-            a += v & kMask;
-            b += v >> kRadixBits;
-          }
-        accA[(size_t)q * g.ncp + c] += a;
-        accB[(size_t)q * g.ncp + c] += b;
+      // two columns per thread; the pair list s_wq is read once into registers
+      uint32_t wmask[kMaxP] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int w = 0; w < nw_used; w++)
+        if (s_wq[w] >= 0) wmask[s_wq[w]] |= 1u << w;
+      const int nh = g.ncp / 2;
+      for (int e = tid; e < p.NP * nh; e += kThreads) {
+        const int q = e / nh, c = 2 * (e - q * nh);
+        int64_t a0 = 0, b0 = 0, a1 = 0, b1 = 0;
+        uint32_t m = q == 0 ? wmask[0] : q == 1 ? wmask[1] : q == 2 ? wmask[2] : wmask[3];
+        while (m) {
+          const int w = __ffs(m) - 1;
+          m &= m - 1;
+          const longlong2 v = *(const longlong2*)(wcol + (size_t)w * g.ncp + c);
+          a0 += v.x & kMask;
+          b0 += v.x >> kRadixBits;
+          a1 += v.y & kMask;
+          b1 += v.y >> kRadixBits;
+        }
+        longlong2* pa = (longlong2*)(accA + (size_t)q * g.ncp + c);
+        longlong2* pb = (longlong2*)(accB + (size_t)q * g.ncp + c);
+        const longlong2 xa = *pa, xb = *pb;
+        *pa = make_longlong2(xa.x + a0, xa.y + a1);
+        *pb = make_longlong2(xb.x + b0, xb.y + b1);
       }
       __syncthreads();
     };
@@ -981,34 +1306,60 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
       for (int r = 1; r <= N; r++) {
         const bool own = owner(r) == o;
         const int rb = r & 3;
+        const bool blog = p.dbg && n == p.start_step + 1 && r < 256 && tid == 0 && o <= 2;
+#define BT(k) \
+  if (blog) p.dbg[40000 + ((size_t)(o - 1) * 256 + r) * 8 + (k)] = (long long)clock64();
+        BT(0);
         if (tid == 0) mbar_expect(&s_bar[rb], row_bytes * (uint32_t)(own ? p.D : nfull));
         mbar_wait(&s_bar[rb], (rph4 >> rb) & 1);
         rph4 ^= 1u << rb;
-        if (warp < p.D && (own || s_full[warp])) {  // nonzero ranges of the rows that arrived
-          const int2 inf = row_info(ROW(warp, r), p.W);
-          if (lane == 0) rinfo[SLOT(warp, r)] = inf;
+        BT(1);
+        if (!bfast) {  // nonzero ranges of the rows that arrived (range-aware products only)
+          if (warp < p.D && (own || s_full[warp])) {
+            const int2 inf = row_info(ROW(warp, r), p.W);
+            if (lane == 0) rinfo[SLOT(warp, r)] = inf;
+          }
+          __syncthreads();
         }
-        __syncthreads();
         // (a) new terms of L'(r+2): k = 2 (rows r, 2) in owner(2); k = r (rows 2, r) in owner(r), r != 2
         if (r >= 2 && r + 2 <= N - 1 && p.NP > 0) {
           int nw = 0;
           for (int q = 0; q < p.NP; q++) {
             const int a = p.pj[q], b = p.pk[q];
             if (owner(2) == o) {
-              if (nw == warp)
-                warp_product<NCH>(s_prod[warp], ROW(a, r), RINF(a, r), ROW(b, 2), RINF(b, 2), g.T, g, wcol + (size_t)nw * g.ncp, mc);
+              if (nw == warp) {
+                if (bzskip)
+                  zs_product(ROW(a, r), p.W, ROW(b, 2), p.W, 0, g.T, bshr, bshg, lrb, s_gl[2], g.ng, bscr,
+                             wcol + (size_t)nw * g.ncp, g.ncols, g.ncp, false, mc);
+                else if (bfast)
+                  lead_product(ROW(a, r), ROW(b, 2), g.T, lrb, s_gl[2], g.ng, bscr, wcol + (size_t)nw * g.ncp, g.ncols,
+                               g.ncp);
+                else
+                  warp_product<NCH>(s_prod[warp], ROW(a, r), RINF(a, r), ROW(b, 2), RINF(b, 2), g.T, g,
+                                    wcol + (size_t)nw * g.ncp, mc);
+              }
               if (tid == 0) s_wq[nw] = q;
               nw++;
             }
             if (r != 2 && own) {
-              if (nw == warp)
-                warp_product<NCH>(s_prod[warp], ROW(a, 2), RINF(a, 2), ROW(b, r), RINF(b, r), g.T, g, wcol + (size_t)nw * g.ncp, mc);
+              if (nw == warp) {
+                if (bzskip)
+                  zs_product(ROW(a, 2), p.W, ROW(b, r), p.W, 0, g.T, bshr, bshg, lrb, s_gl[2], g.ng, bscr,
+                             wcol + (size_t)nw * g.ncp, g.ncols, g.ncp, false, mc);
+                else if (bfast)
+                  lead_product(ROW(a, 2), ROW(b, r), g.T, lrb, s_gl[2], g.ng, bscr, wcol + (size_t)nw * g.ncp, g.ncols,
+                               g.ncp);
+                else
+                  warp_product<NCH>(s_prod[warp], ROW(a, 2), RINF(a, 2), ROW(b, r), RINF(b, r), g.T, g,
+                                    wcol + (size_t)nw * g.ncp, mc);
+              }
               if (tid == 0) s_wq[nw] = q;
               nw++;
             }
           }
           if (nw > 0) absorb(nw);
         }
+        BT(2);
         // (b) push split1(P_o) of L'(r+2) to the lead
         if (r + 2 >= 4 && r + 2 <= N - 1 && p.NP > 0) {
           const int j = r + 2;
@@ -1036,6 +1387,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
           for (int e = tid; e < NPp * g.ncp; e += kThreads) accA[e] = accB[e] = 0;
           __syncthreads();
         }
+        BT(3);
         // (c) old terms of L'(r+3): k in [3, r] owned, rows r+3-k and k
         if (r + 3 <= N - 1 && r >= 3 && p.NP > 0) {
           int kfirst = 3;
@@ -1049,21 +1401,50 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
             if (warp < wpp * p.NP) {
               const int q = warp % p.NP, kw = warp / p.NP;
               const int a = p.pj[q], b = p.pk[q];
-              int np = 0;
-              for (int u = 0; u < kPerWarpPass; u++) {
-                const int kk = base + kw + u * wpp;
-                if (kk >= nk) break;
-                const int k = kfirst + kk * Gb;
-                if (lane == 0) s_prod[warp][u] = mkprod(ROW(a, r + 3 - k), RINF(a, r + 3 - k), ROW(b, k), RINF(b, k));
-                np = u + 1;
+              if (bzskip) {
+                int64_t* outw = wcol + (size_t)warp * g.ncp;
+                for (int c = lane; c < g.ncp; c += 32) outw[c] = 0;
+                __syncwarp();
+#pragma unroll 1
+                for (int u = 0; u < kPerWarpPass; u++) {
+                  const int kk = base + kw + u * wpp;
+                  if (kk >= nk) break;
+                  const int k = kfirst + kk * Gb;
+                  zs_product(ROW(a, r + 3 - k), p.W, ROW(b, k), p.W, 0, g.T, bshr, bshg, lrb, s_gl[2], g.ng, bscr, outw,
+                             g.ncols, g.ncp, true, mc);
+                }
+              } else if (bfast) {
+                int64_t acc[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) acc[u] = 0;
+#pragma unroll 1
+                for (int u = 0; u < kPerWarpPass; u++) {
+                  const int kk = base + kw + u * wpp;
+                  if (kk >= nk) break;
+                  const int k = kfirst + kk * Gb;
+                  run_acc(acc, ROW(a, r + 3 - k), ROW(b, k), g.T, lrb);
+                }
+                run_reduce(acc, s_gl[2], g.ng, bscr, wcol + (size_t)warp * g.ncp, g.ncols, g.ncp);
+              } else {
+                int np = 0;
+                for (int u = 0; u < kPerWarpPass; u++) {
+                  const int kk = base + kw + u * wpp;
+                  if (kk >= nk) break;
+                  const int k = kfirst + kk * Gb;
+                  if (lane == 0) s_prod[warp][u] = mkprod(ROW(a, r + 3 - k), RINF(a, r + 3 - k), ROW(b, k), RINF(b, k));
+                  np = u + 1;
+                }
+                __syncwarp();
+                warp_prods<NCH>(s_prod[warp], np, g.T, g.ng, smem_u32(wcol + (size_t)warp * g.ncp), g.ncp, g.ncols, 0,
+                                mc);
               }
-              __syncwarp();
-              warp_prods<NCH>(s_prod[warp], np, g.T, g.ng, smem_u32(wcol + (size_t)warp * g.ncp), g.ncp, g.ncols, 0, mc);
             }
             absorb(kWarps);
           }
           (void)nprod;
         }
+        BT(4);
+#undef BT
       }
       cluster_barrier();  // [B]
     }

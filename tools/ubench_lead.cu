@@ -1,11 +1,13 @@
 // Micro-benchmark of the mx lead's product stage on one SM (not part of the
-// product): 15 warps x one W-digit truncated product each, as in one order.
+// product): 15 W-digit truncated products, as in one order, with the one-
+// product-per-warp routine (warp_prods) and the several-products-per-warp
+// routine (warp_multi).
 #include <cstdio>
 #include "../paper_1908_09301_b200/csrc/taylor_mx.cu"
 using namespace mpt;
 using namespace mpt::mx;
 
-template <int NCH>
+template <int NCH, int NP2>
 __global__ void __launch_bounds__(512, 1) kb(int W, int reps, long long* out) {
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ Prod slot[16][4];
@@ -28,22 +30,25 @@ __global__ void __launch_bounds__(512, 1) kb(int W, int reps, long long* out) {
   }
   long long t1 = clock64();
   if (tid == 0) out[0] = (t1 - t0) / reps;
+  // several products per warp
+  const int ppw = 32 / (2 * NP2);
+  const int nw = (15 + ppw - 1) / ppw;
+  if (warp < nw && lane < ppw) {
+    const int pi = warp * ppw + lane;
+    if (pi < 15) slot[warp][lane] = mkprod(rows + (pi % 3) * rs, make_int2(0, W - 1), rows + (3 + pi % 8) * rs, make_int2(0, W));
+  }
+  __syncthreads();
   t0 = clock64();
   for (int r = 0; r < reps; r++) {
-    if (warp == 0)
-      warp_product<NCH>(slot[warp], rows, make_int2(0, W - 1), rows + 3 * rs, make_int2(0, W), g.Tc, g, col, nullptr);
+    if (warp < nw) {
+      const int np = min(ppw, 15 - warp * ppw);
+      warp_multi<NP2>(slot[warp], np, g.Tc, g.ng, smem_u32(col + warp * ppw * 128), 128 * 8, g.ncp, g.ncols, nullptr);
+    }
     __syncthreads();
   }
   t1 = clock64();
   if (tid == 0) out[1] = (t1 - t0) / reps;
-  if (warp == 0) {
-    int2 inf;
-    t0 = clock64();
-    bool o = false;
-    for (int r = 0; r < reps; r++) o |= warp_snf_call<2>(col, g.ncols, W, rows + 12 * rs, &inf);
-    t1 = clock64();
-    if (lane == 0) { out[2] = (t1 - t0) / reps; out[7] = o; }
-  }
+  out[2] = nw;
 }
 
 int main() {
@@ -52,16 +57,16 @@ int main() {
   for (int W : {8, 62}) {
     cudaMemset(d, 0, 64);
     if (W == 8) {
-      cudaFuncSetAttribute(kb<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      kb<16><<<1, 512, 200 * 1024>>>(W, 50, d);
+      cudaFuncSetAttribute(kb<16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      kb<16, 1><<<1, 512, 200 * 1024>>>(W, 50, d);
     } else {
-      cudaFuncSetAttribute(kb<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      kb<8><<<1, 512, 200 * 1024>>>(W, 50, d);
+      cudaFuncSetAttribute(kb<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      kb<8, 4><<<1, 512, 200 * 1024>>>(W, 50, d);
     }
     long long h[8];
     cudaError_t e = cudaMemcpy(h, d, 64, cudaMemcpyDeviceToHost);
-    printf("{\"W\": %d, \"products_15warps\": %lld, \"product_1warp\": %lld, \"warp_snf\": %lld, \"err\": \"%s\"}\n", W,
-           h[0], h[1], h[2], cudaGetErrorString(e));
+    printf("{\"W\": %d, \"one_product_per_warp_15\": %lld, \"multi_products_15\": %lld, \"multi_warps\": %lld, \"err\": \"%s\"}\n",
+           W, h[0], h[1], h[2], cudaGetErrorString(e));
   }
   return 0;
 }
