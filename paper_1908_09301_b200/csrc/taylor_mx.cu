@@ -1322,98 +1322,80 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
           __syncthreads();
         }
         // (a) new terms of L'(r+2): k = 2 (rows r, 2) in owner(2); k = r (rows 2, r) in owner(r), r != 2
-        if (r >= 2 && r + 2 <= N - 1 && p.NP > 0) {
-          int nw = 0;
+        const bool push = r >= 2 && r + 2 <= N - 1 && p.NP > 0;
+        int nw = 0;
+        if (push) {
+          if (tid == 0) bulk_wait_read();  // the previous push has read the staging buffer
           for (int q = 0; q < p.NP; q++) {
             const int a = p.pj[q], b = p.pk[q];
-            if (owner(2) == o) {
+            for (int side = 0; side < 2; side++) {
+              const bool mine = side == 0 ? owner(2) == o : (r != 2 && own);
+              if (!mine) continue;
+              const int ra = side == 0 ? r : 2, rb2 = side == 0 ? 2 : r;
               if (nw == warp) {
-                if (bzskip)
-                  zs_product(ROW(a, r), p.W, ROW(b, 2), p.W, 0, g.T, bshr, bshg, lrb, s_gl[2], g.ng, bscr,
-                             wcol + (size_t)nw * g.ncp, g.ncols, g.ncp, false, mc);
-                else if (bfast)
-                  lead_product(ROW(a, r), ROW(b, 2), g.T, lrb, s_gl[2], g.ng, bscr, wcol + (size_t)nw * g.ncp, g.ncols,
-                               g.ncp);
+                if (bfast)
+                  lead_product(ROW(a, ra), ROW(b, rb2), g.T, lrb, s_gl[2], g.ng, bscr, wcol + (size_t)nw * g.ncp,
+                               g.ncols, g.ncp);
                 else
-                  warp_product<NCH>(s_prod[warp], ROW(a, r), RINF(a, r), ROW(b, 2), RINF(b, 2), g.T, g,
-                                    wcol + (size_t)nw * g.ncp, mc);
-              }
-              if (tid == 0) s_wq[nw] = q;
-              nw++;
-            }
-            if (r != 2 && own) {
-              if (nw == warp) {
-                if (bzskip)
-                  zs_product(ROW(a, 2), p.W, ROW(b, r), p.W, 0, g.T, bshr, bshg, lrb, s_gl[2], g.ng, bscr,
-                             wcol + (size_t)nw * g.ncp, g.ncols, g.ncp, false, mc);
-                else if (bfast)
-                  lead_product(ROW(a, 2), ROW(b, r), g.T, lrb, s_gl[2], g.ng, bscr, wcol + (size_t)nw * g.ncp, g.ncols,
-                               g.ncp);
-                else
-                  warp_product<NCH>(s_prod[warp], ROW(a, 2), RINF(a, 2), ROW(b, r), RINF(b, r), g.T, g,
+                  warp_product<NCH>(s_prod[warp], ROW(a, ra), RINF(a, ra), ROW(b, rb2), RINF(b, rb2), g.T, g,
                                     wcol + (size_t)nw * g.ncp, mc);
               }
               if (tid == 0) s_wq[nw] = q;
               nw++;
             }
           }
-          if (nw > 0) absorb(nw);
-        }
-        BT(2);
-        // (b) push split1(P_o) of L'(r+2) to the lead
-        if (r + 2 >= 4 && r + 2 <= N - 1 && p.NP > 0) {
-          const int j = r + 2;
-          int64_t* stg = kcol;  // staging of this CTA's split1(P_o): [q][c]
-          if (tid == 0) bulk_wait_read();  // the previous push has read the staging buffer
           __syncthreads();
-          for (int e = tid; e < p.NP * g.ncp; e += kThreads) {
-            const int q = e / g.ncp, c = e - q * g.ncp;
-            int64_t x = 0;
-            if (c < g.ncols) {
-              x = accA[(size_t)q * g.ncp + c] & kMask;
-              if (c >= 1) x += (accA[(size_t)q * g.ncp + c - 1] >> kRadixBits) + accB[(size_t)q * g.ncp + c - 1];
+          // (b) one pass: P_o = old (accA, accB) + new terms; staging = split1(P_o), two columns per thread
+          // (column c-1 of the pair is recomputed from the raw sums, so no second pass is needed)
+          int64_t* stg = kcol;
+          const int nh = g.ncp / 2;
+          for (int e = tid; e < p.NP * nh; e += kThreads) {
+            const int q = e / nh, c = 2 * (e - q * nh);
+            int64_t A[3], Bc[3];
+#pragma unroll
+            for (int u = 0; u < 3; u++) {
+              const int cc = c - 1 + u;
+              int64_t av = 0, bv = 0;
+              if (cc >= 0 && cc < g.ncols) {
+                av = accA[(size_t)q * g.ncp + cc];
+                bv = accB[(size_t)q * g.ncp + cc];
+                for (int w = 0; w < nw; w++)
+                  if (s_wq[w] == q) {
+                    const int64_t v = wcol[(size_t)w * g.ncp + cc];
+                    av += v & kMask;
+                    bv += v >> kRadixBits;
+                  }
+              }
+              A[u] = av;
+              Bc[u] = bv;
             }
-            stg[e] = x;
+            stg[(size_t)q * g.ncp + c] = c < g.ncols ? (A[1] & kMask) + (A[0] >> kRadixBits) + Bc[0] : 0;
+            stg[(size_t)q * g.ncp + c + 1] = c + 1 < g.ncols ? (A[2] & kMask) + (A[1] >> kRadixBits) + Bc[1] : 0;
           }
           __syncthreads();
           if (tid == 0) {
+            const int j = r + 2;
             fence_async_smem();
             const uint32_t off = (uint32_t)((((size_t)(j & 1) * Gb + (o - 1)) * NPp) * g.ncp * 8);
             bulk_push(mapa_u32(recv_remote + off, 0), smem_u32(stg), (uint32_t)(p.NP * g.ncp * 8),
                       mapa_u32(bar_local + 8 * (j & 1), 0));
             bulk_commit();
           }
-          __syncthreads();
-          for (int e = tid; e < NPp * g.ncp; e += kThreads) accA[e] = accB[e] = 0;
-          __syncthreads();
         }
+        BT(2);
         BT(3);
-        // (c) old terms of L'(r+3): k in [3, r] owned, rows r+3-k and k
-        if (r + 3 <= N - 1 && r >= 3 && p.NP > 0) {
-          int kfirst = 3;
-          while (owner(kfirst) != o) kfirst++;
-          const int nk = kfirst <= r ? (r - kfirst) / Gb + 1 : 0;
-          const int nprod = nk * p.NP;
-          // warps take products round-robin by pair: warp w -> pair w % NP, k index w / NP (+ stride)
-          const int wpp = kWarps / p.NP;  // warps per pair
-          for (int base = 0; base < nk; base += wpp * kPerWarpPass) {
-            if (tid < kWarps) s_wq[tid] = (tid < wpp * p.NP) ? tid % p.NP : -1;
+        // (c) old terms of L'(r+3): k in [3, r] owned, rows r+3-k and k; (accA, accB) are overwritten
+        // whenever the next row pushes (even with no owned k)
+        if (r + 1 >= 2 && r + 3 <= N - 1 && p.NP > 0) {
+          int kfirst = 3 + ((o - 1) - (3 - 1) % Gb + Gb) % Gb;  // smallest k >= 3 with owner(k) == o
+          const int nk = (r >= 3 && kfirst <= r) ? (r - kfirst) / Gb + 1 : 0;
+          const int wpp = kWarps / p.NP;  // warps per pair: warp w -> pair w % NP, k index w / NP (+ stride)
+          if (tid < kWarps) s_wq[tid] = (tid < wpp * p.NP) ? tid % p.NP : -1;
+          for (int base = 0; base == 0 || base < nk; base += wpp * kPerWarpPass) {
             if (warp < wpp * p.NP) {
               const int q = warp % p.NP, kw = warp / p.NP;
               const int a = p.pj[q], b = p.pk[q];
-              if (bzskip) {
-                int64_t* outw = wcol + (size_t)warp * g.ncp;
-                for (int c = lane; c < g.ncp; c += 32) outw[c] = 0;
-                __syncwarp();
-#pragma unroll 1
-                for (int u = 0; u < kPerWarpPass; u++) {
-                  const int kk = base + kw + u * wpp;
-                  if (kk >= nk) break;
-                  const int k = kfirst + kk * Gb;
-                  zs_product(ROW(a, r + 3 - k), p.W, ROW(b, k), p.W, 0, g.T, bshr, bshg, lrb, s_gl[2], g.ng, bscr, outw,
-                             g.ncols, g.ncp, true, mc);
-                }
-              } else if (bfast) {
+              if (bfast) {
                 int64_t acc[8];
 #pragma unroll
                 for (int u = 0; u < 8; u++) acc[u] = 0;
@@ -1439,9 +1421,32 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
                                 mc);
               }
             }
-            absorb(kWarps);
+            __syncthreads();
+            // (A, B) = sums of the warps' low digits / carries; the first pass overwrites
+            const int nh = g.ncp / 2;
+            for (int e = tid; e < p.NP * nh; e += kThreads) {
+              const int q = e / nh, c = 2 * (e - q * nh);
+              int64_t a0 = 0, b0 = 0, a1 = 0, b1 = 0;
+              for (int w = q; w < wpp * p.NP; w += p.NP) {
+                const longlong2 v = *(const longlong2*)(wcol + (size_t)w * g.ncp + c);
+                a0 += v.x & kMask;
+                b0 += v.x >> kRadixBits;
+                a1 += v.y & kMask;
+                b1 += v.y >> kRadixBits;
+              }
+              longlong2* pa = (longlong2*)(accA + (size_t)q * g.ncp + c);
+              longlong2* pb = (longlong2*)(accB + (size_t)q * g.ncp + c);
+              if (base == 0) {
+                *pa = make_longlong2(a0, a1);
+                *pb = make_longlong2(b0, b1);
+              } else {
+                const longlong2 xa = *pa, xb = *pb;
+                *pa = make_longlong2(xa.x + a0, xa.y + a1);
+                *pb = make_longlong2(xb.x + b0, xb.y + b1);
+              }
+            }
+            __syncthreads();
           }
-          (void)nprod;
         }
         BT(4);
 #undef BT
