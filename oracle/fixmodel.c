@@ -306,7 +306,8 @@ static int jet(const model_t *M, int32_t *coef) {
  *   K_i^{m,j'} = rnd_{Lf+2 digits}( tprod(S^{m,j'}, C_i, Lf-2) )  (keeps the sc digits of C_i)
  *   S^{m,j'} = bnf( lin[m][j'] + sum_{t in m, j_t=j'} q_t a~^{k_t}_0 + sum_{t in m, k_t=j'} q_t a~^{j_t}_0 )
  *   lag_t(2) = tprod(a~^a_1, a~^b_1),  lag_t(j>=3) = tprod(a~^a_{j-1}, a~^b_1) + tprod(a~^a_1, a~^b_{j-1})
- *   P_{o,t}(j) = sum_{k in [2, j-2], owner(k) = o} tprod(a~^a_{j-k}, a~^b_k, Lf-2)       (exact)
+ *   P_{o,t}(j) = sum_{k in [2, j-2], own_j(k) = o} tprod(a~^a_{j-k}, a~^b_k, Lf-2)       (exact)
+ *                own_j(k) = owner(k) for k > 2, own_j(2) = owner(j-2) (the newest row's owner)
  *   split1(P)[c] = (P_c mod B) + floor(P_{c-1} / B)   (one carry step, a function of P only)
  *   a~^m_{i+1} = rnd( tprod(U_i^m, C_i, Lf+sc-2) )
  *   U_0 = rnd( cst B^2 + sum_j tprod(lin[m][j], bnf(a~_0^j)) + sum_t q_t tprod(bnf(a~_0^a), bnf(a~_0^b)) )
@@ -421,7 +422,9 @@ static int jet_mx(const model_t *M, int32_t *coef) {
           memset(P, 0, sizeof(i128) * ncols);
           int any = 0;
           for (int k = 2; k <= j - 2; k++) {
-            if (1 + (k - 1) % Gb != o) continue;
+            /* owner(k), except that the k = 2 term goes with the newest row's owner(j-2) */
+            const int ok = k == 2 ? 1 + (j - 3) % Gb : 1 + (k - 1) % Gb;
+            if (ok != o) continue;
             tprod_acc(CO(a, j - k), CO(b, k), L, Lf - 2, P, ncols);
             any = 1;
           }

@@ -146,7 +146,7 @@ __host__ __device__ inline Layout make_layout(const Params& p, int G) {
   L.off_lshg = take(0);
   L.lead_total = o;
   o = 0;
-  L.nslots = row_slots(p, G, -1, nullptr);
+  L.nslots = row_slots(p, G, -1, nullptr) + p.D;  // + row 2 of every variable (the k = 2 Cauchy terms)
   L.off_rows = take(sizeof(int32_t) * ((size_t)L.nslots * g.rs + 3 * kPad));
   L.off_rinfo = take(sizeof(int2) * (size_t)L.nslots);
   L.off_srow = take(sizeof(int32_t) * ((size_t)p.D * p.D * g.rs + 2 * kPad));
@@ -585,7 +585,7 @@ __device__ __noinline__ void warp_multi(const Prod* desc, int nprod, int T, int 
 // compile-time register indices, 8 partial columns to the warp's scratch,
 // and a segment sum per column. Zero digits beyond the operands' nonzero
 // ranges cost MACs but no branches.
-constexpr int kRun = 12;
+constexpr int kRun = 10;
 
 struct LaneRun {
   int g, p0, ns;  // group, first p, steps (0 = idle)
@@ -945,6 +945,11 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
       if (lane == 0) {
         const int sl = SLOT(m, r);
         const uint32_t rb_local = bar_local + 8 * (r & 3);
+        if (r == 2 && !s_full[m]) {  // row 2 of every variable is kept by every bulk CTA
+          const int s2 = L.nslots - p.D + m;
+          bulk_multicast(rows_remote + 4 * s2 * g.rs, gdst, (uint32_t)(g.urs * 4), rb_local,
+                         (uint16_t)(((1u << G) - 1u) & ~1u));
+        }
         if (s_full[m]) {
           bulk_multicast(rows_remote + 4 * sl * g.rs, gdst, (uint32_t)(g.urs * 4), rb_local,
                          (uint16_t)(((1u << G) - 1u) & ~1u));
@@ -1204,6 +1209,9 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
     int64_t* kcol = (int64_t*)(smem + L.off_kcol);
     auto ROW = [&](int v, int k) { return rows + (size_t)SLOT(v, k) * g.rs; };
     auto RINF = [&](int v, int k) { return rinfo[SLOT(v, k)]; };
+    auto ROW2 = [&](int v) {  // row 2 of variable v (every bulk CTA)
+      return s_full[v] ? ROW(v, 2) : rows + (size_t)(L.nslots - p.D + v) * g.rs;
+    };
     const uint32_t recv_remote = smem_u32(smem + L.off_recv);
     const int32_t* lead_state = cluster.map_shared_rank((int32_t*)(smem + L.off_lrow) + 2 * kPad, 0);
     uint32_t rph4 = 0;  // phase bits of the 4 row barriers
@@ -1310,7 +1318,8 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
 #define BT(k) \
   if (blog) p.dbg[40000 + ((size_t)(o - 1) * 256 + r) * 8 + (k)] = (long long)clock64();
         BT(0);
-        if (tid == 0) mbar_expect(&s_bar[rb], row_bytes * (uint32_t)(own ? p.D : nfull));
+        if (tid == 0)
+          mbar_expect(&s_bar[rb], row_bytes * (uint32_t)((own ? p.D : nfull) + (r == 2 ? p.D - nfull : 0)));
         mbar_wait(&s_bar[rb], (rph4 >> rb) & 1);
         rph4 ^= 1u << rb;
         BT(1);
@@ -1329,16 +1338,19 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
           for (int q = 0; q < p.NP; q++) {
             const int a = p.pj[q], b = p.pk[q];
             for (int side = 0; side < 2; side++) {
-              const bool mine = side == 0 ? owner(2) == o : (r != 2 && own);
+              // both new terms (rows r, 2) and (2, r) belong to the newest row's owner
+              const bool mine = own && (side == 0 || r != 2);
               if (!mine) continue;
-              const int ra = side == 0 ? r : 2, rb2 = side == 0 ? 2 : r;
+              const int32_t* A = side == 0 ? ROW(a, r) : ROW(a, 2);
+              const int32_t* Bq = side == 0 ? ROW2(b) : ROW(b, r);
               if (nw == warp) {
                 if (bfast)
-                  lead_product(ROW(a, ra), ROW(b, rb2), g.T, lrb, s_gl[2], g.ng, bscr, wcol + (size_t)nw * g.ncp,
-                               g.ncols, g.ncp);
-                else
-                  warp_product<NCH>(s_prod[warp], ROW(a, ra), RINF(a, ra), ROW(b, rb2), RINF(b, rb2), g.T, g,
-                                    wcol + (size_t)nw * g.ncp, mc);
+                  lead_product(A, Bq, g.T, lrb, s_gl[2], g.ng, bscr, wcol + (size_t)nw * g.ncp, g.ncols, g.ncp);
+                else {
+                  const int2 ia = side == 0 ? RINF(a, r) : RINF(a, 2);
+                  const int2 ib = side == 0 ? (s_full[b] ? RINF(b, 2) : make_int2(0, p.W - 1)) : RINF(b, r);
+                  warp_product<NCH>(s_prod[warp], A, ia, Bq, ib, g.T, g, wcol + (size_t)nw * g.ncp, mc);
+                }
               }
               if (tid == 0) s_wq[nw] = q;
               nw++;
