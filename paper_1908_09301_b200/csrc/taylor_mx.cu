@@ -1105,7 +1105,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
             }
           }
         } else {
-          // aux warp: q_t * sum of the bulk CTAs' L'(j) into lsum[m] (two columns per lane and load)
+          // aux warp: wait for the bulk CTAs' L'(j) (gathered in the column-sum pass below)
           const bool have = doU && j >= 4 && p.NP > 0;
           if (have) {
             const int rp = j & 1;
@@ -1113,45 +1113,42 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
             mbar_wait(&s_bar[rp], (rph >> rp) & 1);
             rph ^= 1u << rp;
           }
-          const int64_t* rv = recv + (size_t)(j & 1) * Gb * NPp * g.ncp;
-          for (int m = 0; m < p.D; m++)
-            for (int c = 2 * lane; c < g.ncp; c += 64) {
-              longlong2 sacc = make_longlong2(0, 0);
-              if (have)
-                for (int t = 0; t < p.NT; t++) {
-                  if (p.teq[t] != m) continue;
-                  const int q = p.tpair[t];
-                  longlong2 v = make_longlong2(0, 0);
-#pragma unroll 4
-                  for (int r = 0; r < Gb; r++) {
-                    const longlong2 x = *(const longlong2*)(rv + ((size_t)r * NPp + q) * g.ncp + c);
-                    v.x += x.x;
-                    v.y += x.y;
-                  }
-                  sacc.x += (int64_t)p.tq_int[t] * v.x;
-                  sacc.y += (int64_t)p.tq_int[t] * v.y;
-                }
-              *(longlong2*)(lsum + (size_t)m * g.ncp + c) = sacc;
-            }
         }
         LT(1);
         __syncthreads();
         LT(2);
-        // ---- roundings: U_j^m (warps 0..D-1), rows a~_{i+1}^m (warps D..2D-1)
+        // ---- column sums of every target on all warps, then the roundings:
+        //      U_j^m (warps 0..D-1), rows a~_{i+1}^m (warps D..2D-1)
+        {
+          const int ntg = 2 * p.D;
+          for (int e = tid; e < ntg * g.ncols; e += kThreads) {
+            const int tg = e / g.ncols, c = e - tg * g.ncols;
+            const bool isU = tg < p.D;
+            if (isU && !doU) continue;
+            const int k0 = s_tr[lk][tg], k1 = s_tr[lk][tg + 1];
+            int64_t sacc = 0;
+            if (isU && doU && j >= 4 && p.NP > 0) {  // q_t * sum over the bulk CTAs of L'_t(j)
+              const int64_t* rv = recv + (size_t)(j & 1) * Gb * NPp * g.ncp;
+              for (int t = 0; t < p.NT; t++) {
+                if (p.teq[t] != tg) continue;
+                const int q = p.tpair[t];
+                int64_t v = 0;
+#pragma unroll 5
+                for (int r = 0; r < Gb; r++) v += rv[((size_t)r * NPp + q) * g.ncp + c];
+                sacc += (int64_t)p.tq_int[t] * v;
+              }
+            }
+            for (int k = k0; k < k1; k++) sacc += (int64_t)s_pl[lk][k].w * cpart[(size_t)k * g.ncp + c];
+            cbuf[(size_t)tg * g.ncp + c] = sacc;
+          }
+        }
+        __syncthreads();
         if (warp < 2 * p.D) {
           const int tg = warp;
           const bool isU = tg < p.D;
           const int m = isU ? tg : tg - p.D;
           if (!isU || doU) {
             int64_t* cv = cbuf + (size_t)tg * g.ncp;
-            const int k0 = s_tr[lk][tg], k1 = s_tr[lk][tg + 1];
-            for (int c = lane; c < g.ncols; c += 32) {
-              int64_t sacc = isU ? lsum[(size_t)m * g.ncp + c] : 0;
-#pragma unroll 4
-              for (int k = k0; k < k1; k++) sacc += (int64_t)s_pl[lk][k].w * cpart[(size_t)k * g.ncp + c];
-              cv[c] = sacc;
-            }
-            __syncwarp();
             const int rr = isU ? R_U + (par ^ 1) * p.D + m : R_ROW + (par ^ 1) * p.D + m;
             if (!isU && lane == 0) bulk_wait_read();  // the owner copy of row i-1 (same buffer) has read it
             __syncwarp();
