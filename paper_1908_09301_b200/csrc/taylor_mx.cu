@@ -700,6 +700,19 @@ __device__ __forceinline__ void run_acc(int64_t (&acc)[8], const int32_t* A, con
   }
 }
 
+// useful (nonzero-range) digit products of this lane's run: for counters only
+__device__ __forceinline__ unsigned long long run_useful(LaneRun lr, int T, int2 ia, int2 ib) {
+  if (lr.ns <= 0 || ia.y < 0 || ib.y < 0) return 0;
+  const int c0 = T + 8 * lr.g;
+  unsigned long long n = 0;
+  for (int r = 0; r < 8; r++) {
+    const int c = c0 + r;
+    const int lo = max(max(ia.x, c - ib.y), lr.p0), hi = min(min(ia.y, c - ib.x), lr.p0 + lr.ns - 1);
+    if (hi >= lo) n += hi - lo + 1;
+  }
+  return n;
+}
+
 // the lanes' windows -> exact columns out[0..ncp) (segment sum per group; `gl` = lane table)
 __device__ __forceinline__ void run_reduce(const int64_t (&acc)[8], const int* gl, int ng, int64_t* scr, int64_t* out,
                                            int nout, int ncp, bool accumulate = false) {
@@ -1097,8 +1110,8 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
               const LaneRun lr = d.x == 0 ? lr0 : (d.x == 1 ? lr1 : lr2);
               lead_product(A, B, T, lr, s_gl[d.x], g.ng, scr, cpart + (size_t)pi * g.ncp, g.ncols, g.ncp);
               if (mc) {
-                if (lane == s_gl[d.x][lr.g]) mcount.useful += group_macs(ia, ib, T + 8 * lr.g);
-                mcount.executed += 8ull * lr.ns;
+                mcount.useful += run_useful(lr, T, ia, ib);
+                mcount.executed += 8ull * kRun;
               }
             } else {
               warp_product<NCH>(s_prod[warp], A, ia, B, ib, T, g, cpart + (size_t)pi * g.ncp, mc);
@@ -1341,8 +1354,13 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
               const int32_t* A = side == 0 ? ROW(a, r) : ROW(a, 2);
               const int32_t* Bq = side == 0 ? ROW2(b) : ROW(b, r);
               if (nw == warp) {
-                if (bfast)
+                if (bfast) {
                   lead_product(A, Bq, g.T, lrb, s_gl[2], g.ng, bscr, wcol + (size_t)nw * g.ncp, g.ncols, g.ncp);
+                  if (mc) {
+                    mcount.useful += run_useful(lrb, g.T, make_int2(0, row_top(A, p.W)), make_int2(0, row_top(Bq, p.W)));
+                    mcount.executed += 8ull * kRun;
+                  }
+                }
                 else {
                   const int2 ia = side == 0 ? RINF(a, r) : RINF(a, 2);
                   const int2 ib = side == 0 ? (s_full[b] ? RINF(b, 2) : make_int2(0, p.W - 1)) : RINF(b, r);
@@ -1414,6 +1432,11 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
                   if (kk >= nk) break;
                   const int k = kfirst + kk * Gb;
                   run_acc(acc, ROW(a, r + 3 - k), ROW(b, k), g.T, lrb);
+                  if (mc) {
+                    mcount.useful += run_useful(lrb, g.T, make_int2(0, row_top(ROW(a, r + 3 - k), p.W)),
+                                                make_int2(0, row_top(ROW(b, k), p.W)));
+                    mcount.executed += 8ull * kRun;
+                  }
                 }
                 run_reduce(acc, s_gl[2], g.ng, bscr, wcol + (size_t)warp * g.ncp, g.ncols, g.ncp);
               } else {
