@@ -280,7 +280,28 @@ def run_b200(args, rank, world, local_rank):
     if rank == 0:
         # ---- e2e: the public drop-in API with host MPValues (plan setup, H2D, kernel, D2H)
         e2e = None
-        if not args.no_e2e:
+        if not args.no_e2e and w["strong"]:
+            # ensemble: the public ensemble entry point with host decimal initial conditions
+            # (parse -> digits -> H2D -> kernel -> D2H of the recorded states), this rank's shard
+            from paper_1908_09301_b200 import ensemble as E
+
+            lo, hi = E.shard_bounds(w["n_total"], world, rank)
+            inits = E.perturbed_inits(w["n_total"], seed=0)[lo:hi]
+            reps = max(1, min(args.steps, args.e2e_reps))
+            E.run_members("lorenz", inits, w["P"], w["N"], w["tau_text"], S, S, device=device)  # warm
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                E.run_members("lorenz", inits, w["P"], w["N"], w["tau_text"], S, S, device=device)
+            dt = (time.perf_counter() - t0) / reps
+            RS, D, N, M = (w["fmt"].width + 3) // 4 * 4, 3, w["N"], hi - lo
+            h2d = 4 * RS * (D + D * D + 2 + N) + 4 * RS * D * M
+            d2h = 4 * w["fmt"].width * D * M * 2 + 4 * M  # records at steps 0 and S, status
+            e2e = {"value": S * M * world / dt, "unit": "taylor_steps/s", "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": d2h,
+                   "how": f"paper_1908_09301_b200.ensemble.run_members(...) of {S} Taylor steps on {M} "
+                          f"members (decimal inits, seed 0), wall clock incl. parsing and plan setup, mean "
+                          f"of {reps}; x{world} ranks"}
+        elif not args.no_e2e:
             ctx, system = w["ctx"], w["system"]
             st = tuple(M.MPValue.from_fraction(f, w["P"]) for f in w["fmt"].digits_to_fractions(w["states"][0]))
             cfg = M.StepConfig(w["tau_text"], w["N"])

@@ -321,6 +321,31 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
     delete pl;
     return fail(MPT_EUNSUP, "shared memory budget exceeded");
   }
+  // Ensembles (the team kernel, one CTA per trajectory): with enough
+  // trajectories to fill every SM twice, size the register budget and the
+  // k-chunk for two resident CTAs per SM so that one trajectory's barriers and
+  // HBM row loads overlap another's products. MPT_TEAM_MB=1 turns it off.
+  p.team_mb = 1;
+  {
+    int nsm = 0, smem_sm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+    const char* em = getenv("MPT_TEAM_MB");
+    const int want_mb = em ? atoi(em) : (n_traj >= 2 * nsm ? 2 : 1);
+    if (want_mb >= 2 && p.NP <= 2) {
+      const size_t cap = (size_t)smem_sm / 2 - 1024;  // 1 KB per CTA is reserved by the runtime
+      const int kc1 = p.kc;
+      for (int k2 = kc1; k2 >= 1; k2 = k2 > 8 ? k2 - 8 : k2 - 1) {
+        p.kc = k2;
+        if (mpt::smem_bytes(p) <= cap) {
+          p.team_mb = 2;
+          smem = mpt::smem_bytes(p);
+          break;
+        }
+      }
+      if (p.team_mb != 2) p.kc = kc1;
+    }
+  }
   pl->smem = smem;
   size_t rows = (size_t)n_traj * dim * (order + 1);
 #define ALLOC(ptr, bytes)                                                         \

@@ -59,6 +59,7 @@ struct Params {
   int n_steps, start_step, stride;
   int kc;               // k values staged per chunk
   int nthreads;
+  int team_mb;          // team kernel: CTAs per SM (1 or 2; ensembles)
   unsigned long long* counters;  // optional: [0] useful limb-MACs, [1] executed limb-MACs
   int write_coef;                // cluster kernel: also store every coefficient row to `coef`
   long long* dbg;                // debug dump (nullptr in production)

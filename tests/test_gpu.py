@@ -112,6 +112,28 @@ def test_ensemble_of_trajectories_bit_exact(gpu):
         assert np.array_equal(r_gpu[:, j], r_cpu), j
 
 
+@pytest.mark.parametrize("mb", ["1", "2"])
+@pytest.mark.parametrize("K,N,steps", [(100, 60, 6), (400, 240, 2)])
+def test_team_kernel_two_ctas_per_sm_bit_exact(gpu, monkeypatch, mb, K, N, steps):
+    """Ensemble team kernel at one and two resident CTAs per SM (the k-chunk
+    shrinks to fit two CTAs' shared memory): every member bit-exact vs the model."""
+    monkeypatch.setenv("MPT_TEAM_MB", mb)
+    P = M.bits_for_digits(K)
+    n_traj = 7
+    ctx, system, fmt, tables = lorenz_tables(P, N)
+    base = [M.mp_from_decimal(t, ctx).as_fraction() for t in CANON_INIT]
+    states = np.stack([fmt.to_digits([b + Fraction(3 * j - 9, 10**20) for b in base]) for j in range(n_traj)])
+    with DevicePlan(tables, fmt, N, n_traj) as plan:
+        plan.configure("team", 1)
+        assert plan.info()["kernel"] == "team"
+        _, r_gpu, status = plan.integrate(states, steps, 0, 1)
+        kw = plan.model_kwargs()
+    assert not status.any()
+    for j in (0, 3, n_traj - 1):
+        _, r_cpu = FX.integrate(tables, fmt.frac_digits, N, P, states[j], steps, 0, 1, **kw)
+        assert np.array_equal(r_gpu[:, j], r_cpu), j
+
+
 def test_random_quadratic_systems_jets_bit_exact(golden, gpu):
     for name, c in golden.items():
         if not name.startswith("random_jet"):
