@@ -29,8 +29,9 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def build(verbose: bool = False, extra=()) -> str:
-    """Compile every translation unit in parallel (-c), then link the .so."""
+def build(verbose: bool = False, extra=(), incremental: bool = False) -> str:
+    """Compile every translation unit in parallel (-c), then link the .so.
+    incremental=True reuses objects newer than their source and the headers."""
     from concurrent.futures import ThreadPoolExecutor
 
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
@@ -39,8 +40,17 @@ def build(verbose: bool = False, extra=()) -> str:
     common = [nvcc(), "-O3", "-lineinfo", "-std=c++17", *ARCH, "-Xcompiler", "-fPIC",
               "-I", os.path.join(REPO, "include"), *(["-Xptxas", "-v"] if verbose else []), *extra]
 
+    csrc = os.path.join(HERE, "csrc")
+    deps = [os.path.join(csrc, f) for f in os.listdir(csrc) if f.endswith(".cuh")]
+    deps.append(os.path.join(REPO, "include", "mptaylor_b200.h"))
+    dep_mtime = max(os.path.getmtime(d) for d in deps)
+
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
+        # incremental: an object newer than its source and every header is reused
+        if (incremental and os.path.exists(obj)
+                and os.path.getmtime(obj) > max(os.path.getmtime(os.path.join(HERE, src)), dep_mtime)):
+            return obj, ""
         res = subprocess.run([*common, "-c", "-o", obj, os.path.join(HERE, src)], capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{res.stdout}\n{res.stderr}")
@@ -59,4 +69,4 @@ def build(verbose: bool = False, extra=()) -> str:
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    print(build(verbose="-v" in sys.argv, incremental="-i" in sys.argv))

@@ -72,6 +72,7 @@ struct mpt_plan {
   int cluster = 1;   // CTAs per trajectory for the cluster kernel
   size_t smem_cluster = 0;
   int optin = 0;
+  int nsm = 148;     // SMs of the device
   int requested_kernel = 0, requested_cluster = 1;
   int grid_blocks = 0, grid_kc = 0;
   size_t smem_grid = 0;
@@ -173,6 +174,13 @@ static int choose_kernel(mpt_plan* pl, int kernel, int want) {
       return MPT_OK;
     }
     return fail(MPT_EUNSUP, "the relay kernel does not support this system/precision (shared memory)");
+  }
+  // ensembles that fill every SM: one trajectory per CTA (team kernel, two
+  // CTAs per SM) beats a per-trajectory cluster (measured ens100-ens800)
+  if (kernel == 0 && p.n_traj >= pl->nsm) {
+    pl->kernel = 1;
+    pl->cluster = 1;
+    return MPT_OK;
   }
   // the pipelined kernel needs the constants (integer bilinear coefficients)
   if ((kernel == 0 || kernel == 3) && pl->have_constants && mpt::pipe_supported(p)) {
@@ -329,6 +337,7 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
   {
     int nsm = 0, smem_sm = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    pl->nsm = nsm;
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
     const char* em = getenv("MPT_TEAM_MB");
     const int want_mb = em ? atoi(em) : (n_traj >= 2 * nsm ? 2 : 1);

@@ -64,7 +64,7 @@ __host__ __device__ inline Layout make_layout(const Params& p) {
   L.rw = row_words(p.RS);
   L.n_stage_rows = p.kc * (p.nlv + p.nrv);
   L.n_const_rows = p.D + p.D * p.D + p.NT;
-  int ns = p.nthreads / g.NGb;
+  int ns = p.nthreads / ((p.NP > 0 ? p.NP : 1) * ((g.NGb + 1) / 2));
   if (ns < 1) ns = 1;
   int units_a = ns * (p.NP > 0 ? p.NP : 1);
   int units_b = p.D * p.D + p.NT;  // numerator items
@@ -173,7 +173,10 @@ __global__ void __launch_bounds__(256, MB) taylor_team_kernel(const __grid_const
   for (int m = 0; m < p.D; m++) copy_row(ROW(cur, m), gstate + (size_t)m * p.RS, p.RS);
   __syncthreads();
 
-  const int ns_a = max(1, nt / g.NGb);  // k slots in phase A
+  // phase A units: (k slot, pair, group pair) -- see team_units()
+  const int NGh = (g.NGb + 1) / 2;
+  const int unit_per_slot = max(1, p.NP) * NGh;
+  const int ns_a = max(1, nt / unit_per_slot);  // k slots in phase A
   int status = 0;
   MacCount mcount;
   MacCount* mc = p.counters ? &mcount : nullptr;
@@ -202,16 +205,20 @@ __global__ void __launch_bounds__(256, MB) taylor_team_kernel(const __grid_const
     for (int i = 0; i < p.N; i++) {
       // ===================== phase A: Cauchy sums =====================
       if (p.NP > 0) {
-        const int slot = tid / g.NGb, grp = tid % g.NGb;
+        // unit = (slot, pair q, group pair h): the thread accumulates column
+        // windows h and NGb-1-h of pair q. Low windows hold ~W digit products
+        // per column, high ones few; pairing them gives every lane the same
+        // work (a warp runs at its slowest lane).
+        const int slot = tid / unit_per_slot, rem = tid % unit_per_slot;
+        const int q = rem / NGh, h = rem % NGh;
         const bool active = slot < ns_a;
-        const int c0 = kR * (g.gfb + grp);
-        Acc acc[NPT];
-        int cnt[NPT];
-#pragma unroll
-        for (int q = 0; q < NPT; q++) {
-          acc_zero(acc[q]);
-          cnt[q] = 0;
-        }
+        const int gB = g.NGb - 1 - h;
+        const bool twoB = gB != h;
+        const int c0A = kR * (g.gfb + h), c0B = kR * (g.gfb + gB);
+        Acc accA, accB;
+        acc_zero(accA);
+        acc_zero(accB);
+        int cntA = 0, cntB = 0;
         const int nrows = p.nlv + p.nrv;
         for (int k0 = 0; k0 <= i; k0 += p.kc) {
           const int kcn = min(p.kc, i + 1 - k0);
@@ -240,43 +247,39 @@ __global__ void __launch_bounds__(256, MB) taylor_team_kernel(const __grid_const
           __syncthreads();
           if (active) {
             for (int kk = slot; kk < kcn; kk += ns_a) {
-#pragma unroll
-              for (int q = 0; q < NPT; q++) {
-                if (q < p.NP) {
-                  const int ra = kk * nrows + p.pl[q];
-                  const int rb = kk * nrows + p.nlv + p.pr[q];
-                  mac_group(acc[q], cnt[q], ROW(stage, ra), stinfo[ra], ROW(stage, rb), stinfo[rb], c0, g.Tb, mc);
-                }
-              }
+              const int ra = kk * nrows + p.pl[q];
+              const int rb = kk * nrows + p.nlv + p.pr[q];
+              mac_group(accA, cntA, ROW(stage, ra), stinfo[ra], ROW(stage, rb), stinfo[rb], c0A, g.Tb, mc);
+              if (twoB)
+                mac_group(accB, cntB, ROW(stage, ra), stinfo[ra], ROW(stage, rb), stinfo[rb], c0B, g.Tb, mc);
             }
           }
           __syncthreads();
         }
         // partials: unit = slot * NP + q, columns relative to Tb
         if (active) {
+          int64_t* pr = part + (size_t)(slot * p.NP + q) * g.NCX;
+          acc_fold(accA, c0A, g.Tb);
 #pragma unroll
-          for (int q = 0; q < NPT; q++) {
-            if (q < p.NP) {
-              acc_fold(acc[q], c0, g.Tb);
-              int64_t* pr = part + (size_t)(slot * p.NP + q) * g.NCX;
+          for (int r = 0; r < kR; r++) {
+            int c = c0A + r - g.Tb;
+            if (c >= 0) pr[c] = accA.v[r];
+          }
+          if (twoB) {
+            acc_fold(accB, c0B, g.Tb);
 #pragma unroll
-              for (int r = 0; r < kR; r++) {
-                int c = c0 + r - g.Tb;
-                if (c >= 0) pr[c] = acc[q].v[r];
-              }
+            for (int r = 0; r < kR; r++) {
+              int c = c0B + r - g.Tb;
+              if (c >= 0) pr[c] = accB.v[r];
             }
           }
         }
         for (int u = tid; u < ns_a * p.NP; u += nt) uout[u] = u % p.NP;
         __syncthreads();
         if (active) {
-#pragma unroll
-          for (int q = 0; q < NPT; q++) {
-            if (q < p.NP) {
-              int c = c0 + kR - g.Tb;
-              part[(size_t)(slot * p.NP + q) * g.NCX + c] += acc[q].v[kR];
-            }
-          }
+          int64_t* pr = part + (size_t)(slot * p.NP + q) * g.NCX;
+          pr[c0A + kR - g.Tb] += accA.v[kR];  // carries land in distinct columns (h+1 <= NGb-h)
+          if (twoB) pr[c0B + kR - g.Tb] += accB.v[kR];
         }
         __syncthreads();
         // reduce units -> colsum[q][c]
