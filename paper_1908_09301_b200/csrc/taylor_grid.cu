@@ -64,6 +64,13 @@ __host__ __device__ inline int lin_slot(const Params& p, int it) {
   return s;
 }
 
+// phase A k slots: a slot is NP x ceil(NGb/2) lanes, one per (pair q, window
+// pair h): each lane accumulates the windows h and NGb-1-h (balanced work)
+__host__ __device__ inline int grid_slots(const Params& p, const Geo& g) {
+  const int per = (p.NP > 0 ? p.NP : 1) * ((g.NGb + 1) / 2);
+  return kThreads / per > 0 ? kThreads / per : 1;
+}
+
 // crow: cst D | lin D*D | q NT | ctab | U D | CUR D
 __host__ __device__ inline Layout make_layout(const Params& p, int kc) {
   Layout L;
@@ -72,7 +79,7 @@ __host__ __device__ inline Layout make_layout(const Params& p, int kc) {
   L.kc = kc;
   L.nrows = p.nlv + p.nrv;
   L.ncrow = p.D + p.D * p.D + p.NT + 1 + 2 * p.D;
-  const int ns = kThreads / g.NGb > 0 ? kThreads / g.NGb : 1;
+  const int ns = grid_slots(p, g);
   int nu = ns * (p.NP > 0 ? p.NP : 1) + kLinPC * lin_slot(p, p.D * p.D);
   if (p.D * kPC > nu) nu = p.D * kPC;
   L.nunits = nu;
@@ -211,8 +218,11 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
   MacCount mcount;
   MacCount* mc = p.counters ? &mcount : nullptr;
   const int nlin = p.D * p.D;
-  const int ns = kThreads / g.NGb;
-  const int slot = tid / g.NGb, grp = tid - slot * g.NGb;
+  const int ns = grid_slots(p, g);
+  const int NGh = (g.NGb + 1) / 2;
+  const int unit_per_slot = (p.NP > 0 ? p.NP : 1) * NGh;
+  const int slot = tid / unit_per_slot, urem = tid - slot * unit_per_slot;
+  const int qa = urem / NGh, ha = urem - qa * NGh;  // phase A: pair qa, windows ha and NGb-1-ha
 
   for (int n = p.start_step + 1; n <= p.n_steps; n++) {
     // order 0 rows = state (every CTA holds it; CTA 0 publishes it)
@@ -237,14 +247,13 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
       unsigned long long* ca = cacc + (size_t)buf * p.D * g.NCX;
       // ================= phase A: Cauchy terms k = b (mod nb), staged kc at a time
       if (p.NP > 0) {
-        Acc acc[NPT];
-        int cnt[NPT];
-#pragma unroll
-        for (int q = 0; q < NPT; q++) {
-          acc_zero(acc[q]);
-          cnt[q] = 0;
-        }
-        const int c0 = kR * (g.gfb + grp);
+        Acc accA, accB;
+        acc_zero(accA);
+        acc_zero(accB);
+        int cntA = 0, cntB = 0;
+        const int gB = g.NGb - 1 - ha;
+        const bool twoB = gB != ha;
+        const int c0A = kR * (g.gfb + ha), c0B = kR * (g.gfb + gB);
         const int nk = b <= i ? (i - b) / nb + 1 : 0;  // this CTA's k values
         // few k values: split every product's p range over several slots
         const int pch = nk > 0 ? max(1, min(16, ns / min(nk, kc))) : 1;
@@ -282,25 +291,21 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_grid_kernel(const __grid_c
           if (slot < ns) {
             for (int wu = slot; wu < kcn * pch; wu += ns) {
               const int kk = wu / pch, pc = wu - kk * pch;
-#pragma unroll
-              for (int q = 0; q < NPT; q++) {
-                if (q < p.NP) {
-                  const int ra = kk * L.nrows + p.pl[q], rb = kk * L.nrows + p.nlv + p.pr[q];
-                  mac_group_chunk(acc[q], cnt[q], SROW(ra), stinfo[ra], SROW(rb), stinfo[rb], c0, g.Tb, pc, pch, mc);
-                }
-              }
+              const int ra = kk * L.nrows + p.pl[qa], rb = kk * L.nrows + p.nlv + p.pr[qa];
+              mac_group_chunk(accA, cntA, SROW(ra), stinfo[ra], SROW(rb), stinfo[rb], c0A, g.Tb, pc, pch, mc);
+              if (twoB)
+                mac_group_chunk(accB, cntB, SROW(ra), stinfo[ra], SROW(rb), stinfo[rb], c0B, g.Tb, pc, pch, mc);
             }
           }
           __syncthreads();
         }
         if (slot < ns) {
-#pragma unroll
-          for (int q = 0; q < NPT; q++) {
-            if (q < p.NP) {
-              acc_fold(acc[q], c0, g.Tb);
-              const int u = slot * p.NP + q;
-              store_unit(part + (size_t)u * g.NCX, pcar + (size_t)u * L.ngmax, acc[q], grp, c0, g.Tb);
-            }
+          const int u = slot * p.NP + qa;
+          acc_fold(accA, c0A, g.Tb);
+          store_unit(part + (size_t)u * g.NCX, pcar + (size_t)u * L.ngmax, accA, ha, c0A, g.Tb);
+          if (twoB) {
+            acc_fold(accB, c0B, g.Tb);
+            store_unit(part + (size_t)u * g.NCX, pcar + (size_t)u * L.ngmax, accB, gB, c0B, g.Tb);
           }
         }
       }
