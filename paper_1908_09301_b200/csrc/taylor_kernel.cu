@@ -358,26 +358,46 @@ __global__ void __launch_bounds__(256, MB) taylor_team_kernel(const __grid_const
         }
         __syncthreads();
         for (size_t w = tid; w < (size_t)nitems * g.NCX; w += nt) part[w] = 0;
-        // tau/(i+1) row for phase C
-        copy_row(ROW(ctrow, 0), p.ctab + (size_t)i * p.RS, p.RS);
+        // tau/(i+1) row for phase C: staged (with its digit range) by a warp
+        // that has no normalisation to do, in the same barrier phase
+        const int ctw = p.D < nwarps ? p.D : -1;
+        if (ctw < 0) copy_row(ROW(ctrow, 0), p.ctab + (size_t)i * p.RS, p.RS);
         for (int m = warp; m < p.D; m += nwarps) {
           bool o = warp_normalize(ucol + (size_t)m * g.NCX, ncol, 2, p.W, ROW(urow, m), &uinf[m], 0);
           if (o && (tid & 31) == 0) flag[0] = 1;
         }
-        __syncthreads();
-        if (warp == 0) {
+        if (warp == ctw) {
           int bot = 1 << 30, tp = -1;
-          const int32_t* row = ROW(ctrow, 0);
-          for (int d = (tid & 31); d < p.W; d += 32)
-            if (row[d]) {
+          int32_t* row = ROW(ctrow, 0);
+          const int32_t* src = p.ctab + (size_t)i * p.RS;
+          for (int d = (tid & 31); d < p.RS; d += 32) {
+            const int32_t v = src[d];
+            row[d] = v;
+            if (d < p.W && v) {
               bot = min(bot, d);
               tp = max(tp, d);
             }
+          }
           bot = __reduce_min_sync(0xffffffffu, bot);
           tp = __reduce_max_sync(0xffffffffu, tp);
-          if (tid == 0) ctinf[0] = make_int2(tp >= 0 ? bot : p.W, tp);
+          if ((tid & 31) == 0) ctinf[0] = make_int2(tp >= 0 ? bot : p.W, tp);
         }
         __syncthreads();
+        if (ctw < 0) {
+          if (warp == 0) {
+            int bot = 1 << 30, tp = -1;
+            const int32_t* row = ROW(ctrow, 0);
+            for (int d = (tid & 31); d < p.W; d += 32)
+              if (row[d]) {
+                bot = min(bot, d);
+                tp = max(tp, d);
+              }
+            bot = __reduce_min_sync(0xffffffffu, bot);
+            tp = __reduce_max_sync(0xffffffffu, tp);
+            if (tid == 0) ctinf[0] = make_int2(tp >= 0 ? bot : p.W, tp);
+          }
+          __syncthreads();
+        }
       }
       // ===================== phase C: scale by tau/(i+1) =====================
       {
