@@ -75,18 +75,23 @@ class FixedFormat:
     def ints_to_digits(self, xs) -> np.ndarray:
         """Signed integers -> int32 digit rows (len(xs) x W)."""
         W = self.width
-        out = np.zeros((len(xs), W), dtype=np.int32)
+        xs = [int(x) for x in xs]
+        if not xs:
+            return np.zeros((0, W), dtype=np.int32)
         nbytes = (RADIX_BITS * W + 7) // 8 + 1
-        for r, x in enumerate(xs):
-            mag = abs(int(x))
-            if mag >> (RADIX_BITS * W):
-                raise RangeError("value exceeds the digit width")
-            bits = np.unpackbits(
-                np.frombuffer(mag.to_bytes(nbytes, "little"), dtype=np.uint8), bitorder="little"
-            )[: RADIX_BITS * W].reshape(W, RADIX_BITS)
-            d = bits.astype(np.int64) @ (np.int64(1) << np.arange(RADIX_BITS, dtype=np.int64))
-            out[r] = (-d if x < 0 else d).astype(np.int32)
-        return out
+        mags = [abs(x) for x in xs]
+        if any(m >> (RADIX_BITS * W) for m in mags):
+            raise RangeError("value exceeds the digit width")
+        # all rows at once: little-endian bytes -> bits -> radix-2^28 digits
+        raw = np.frombuffer(b"".join(m.to_bytes(nbytes + 4, "little") for m in mags), dtype=np.uint8)
+        raw = raw.reshape(len(xs), nbytes + 4).astype(np.int64)
+        off = RADIX_BITS * np.arange(W)
+        b0, sh = off // 8, off % 8  # digit j = 4 bytes from byte b0, shifted right by sh
+        word = raw[:, b0] | (raw[:, b0 + 1] << 8) | (raw[:, b0 + 2] << 16) | (raw[:, b0 + 3] << 24) | (
+            raw[:, b0 + 4] << 32)
+        d = (word >> sh) & ((1 << RADIX_BITS) - 1)
+        neg = np.fromiter((x < 0 for x in xs), dtype=bool, count=len(xs))
+        return np.ascontiguousarray(np.where(neg[:, None], -d, d), dtype=np.int32)
 
     def digits_to_ints(self, rows) -> list:
         """Digit rows -> integers. Canonical rows (every digit carries the

@@ -86,3 +86,27 @@ def test_signed_zero_and_bits_equal():
     assert nz.is_zero() and nz.is_signed()
     assert not M.mp_bits_equal(nz, ctx.zero)
     assert M.mp_to_decimal(nz, 3) == "-0.00"
+
+
+@pytest.mark.parametrize("K", [50, 500, 4200])
+def test_digit_rows_round_trip(K):
+    """Batched int -> radix-2^28 digit rows (the H2D format) and back, with the
+    width edges; values past the width raise like the reference's range errors."""
+    import numpy as np
+
+    from paper_1908_09301_b200.fixed import FixedFormat
+
+    fmt = FixedFormat(M.bits_for_digits(K))
+    top = (1 << (28 * fmt.width)) - 1
+    rng = random.Random(K)
+    xs = [rng.randint(-(1 << (fmt.frac_bits + 20)), 1 << (fmt.frac_bits + 20)) for _ in range(200)]
+    xs += [0, 1, -1, top, -top, 1 << 27, -(1 << 28)]
+    d = fmt.ints_to_digits(xs)
+    assert d.dtype == np.int32 and d.shape == (len(xs), fmt.width) and d.flags.c_contiguous
+    assert (np.abs(d) < (1 << 28)).all()
+    assert fmt.digits_to_ints(d) == xs
+    for r, x in zip(d[:20], xs[:20]):  # digit-by-digit definition
+        assert sum(int(v) << (28 * j) for j, v in enumerate(r)) == x
+    assert fmt.ints_to_digits([]).shape == (0, fmt.width)
+    with pytest.raises(M.RangeError):
+        fmt.ints_to_digits([top + 1])
