@@ -344,12 +344,8 @@ __global__ void __launch_bounds__(256, MB) taylor_team_kernel(const __grid_const
         for (int e = tid; e < p.D * ncol; e += nt) {
           const int m = e / ncol, c = e % ncol;
           int64_t s = 0;
-          // only product items exist in `part` (small-integer ones were skipped
-          // and their rows are zero): test the uniform parameters, not smem
-          for (int u = m * p.D; u < (m + 1) * p.D; u++)
-            if (!p.lin_small[u]) s += part[(size_t)u * g.NCX + c];
-          for (int t = 0; t < p.NT; t++)
-            if (!p.tq_small[t] && p.teq[t] == m) s += part[(size_t)(nlin + t) * g.NCX + c];
+          for (int u = 0; u < nitems; u++)
+            if (uout[u] == m) s += part[(size_t)u * g.NCX + c];
           if (c >= 2 && c - 2 < p.W) {
             const int dgt = c - 2;
             if (i == 0) s += ROW(crow, m)[dgt];
