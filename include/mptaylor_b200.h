@@ -73,7 +73,7 @@ int mpt_plan_destroy(mpt_plan *plan);
  *         4 grid kernel (one trajectory on every SM, rows in L2; large precision);
  * cluster: CTAs per trajectory (1..16) for the cluster kernel.
  * Environment overrides at plan creation: MPT_KERNEL=team|cluster|pipe|grid, MPT_CLUSTER=G,
- * MPT_TEAM_MB=1|2 (team kernel CTAs per SM; default 2 when n_traj >= 2 x SMs). */
+ * MPT_TEAM_MB=1|2|4 (team kernel CTAs per SM; default 4 (128 threads) when n_traj >= 4 x SMs and W <= 64, else 2 when n_traj >= 2 x SMs). */
 int mpt_plan_configure(mpt_plan *plan, int kernel, int cluster);
 int mpt_plan_kernel(const mpt_plan *plan, int *kernel, int *cluster);
 

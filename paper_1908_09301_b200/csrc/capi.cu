@@ -340,19 +340,24 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
     pl->nsm = nsm;
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
     const char* em = getenv("MPT_TEAM_MB");
-    const int want_mb = em ? atoi(em) : (n_traj >= 2 * nsm ? 2 : 1);
-    if (want_mb >= 2 && p.NP <= 2) {
-      const size_t cap = (size_t)smem_sm / 2 - 1024;  // 1 KB per CTA is reserved by the runtime
-      const int kc1 = p.kc;
+    // four 128-thread CTAs per SM for small digit counts (latency bound), two otherwise
+    const int want_mb = em ? atoi(em) : (n_traj >= 4 * nsm && p.W <= 64 ? 4 : n_traj >= 2 * nsm ? 2 : 1);
+    const int kc1 = p.kc;
+    for (int mb = want_mb >= 4 ? 4 : want_mb; mb >= 2 && p.NP <= 2 && p.team_mb == 1; mb /= 2) {
+      const size_t cap = (size_t)smem_sm / mb - 1024;  // 1 KB per CTA is reserved by the runtime
+      p.nthreads = mb >= 4 ? 128 : 256;
       for (int k2 = kc1; k2 >= 1; k2 = k2 > 8 ? k2 - 8 : k2 - 1) {
         p.kc = k2;
         if (mpt::smem_bytes(p) <= cap) {
-          p.team_mb = 2;
+          p.team_mb = mb;
           smem = mpt::smem_bytes(p);
           break;
         }
       }
-      if (p.team_mb != 2) p.kc = kc1;
+    }
+    if (p.team_mb == 1) {
+      p.kc = kc1;
+      p.nthreads = 256;
     }
   }
   pl->smem = smem;
