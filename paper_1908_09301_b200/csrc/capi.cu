@@ -341,11 +341,11 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
     const char* em = getenv("MPT_TEAM_MB");
     // four 128-thread CTAs per SM for small digit counts (latency bound), two otherwise
-    const int want_mb = em ? atoi(em) : (n_traj >= 4 * nsm && p.W <= 64 ? 4 : n_traj >= 2 * nsm ? 2 : 1);
+    const int want_mb = em ? atoi(em) : (n_traj >= 8 * nsm && p.W <= 20 ? 8 : n_traj >= 4 * nsm && p.W <= 64 ? 4 : n_traj >= 2 * nsm ? 2 : 1);
     const int kc1 = p.kc;
-    for (int mb = want_mb >= 4 ? 4 : want_mb; mb >= 2 && p.NP <= 2 && p.team_mb == 1; mb /= 2) {
+    for (int mb = want_mb >= 8 ? 8 : want_mb >= 4 ? 4 : want_mb; mb >= 2 && p.NP <= 2 && p.team_mb == 1; mb /= 2) {
       const size_t cap = (size_t)smem_sm / mb - 1024;  // 1 KB per CTA is reserved by the runtime
-      p.nthreads = mb >= 4 ? 128 : 256;
+      p.nthreads = mb >= 8 ? 64 : mb >= 4 ? 128 : 256;
       for (int k2 = kc1; k2 >= 1; k2 = k2 > 8 ? k2 - 8 : k2 - 1) {
         p.kc = k2;
         if (mpt::smem_bytes(p) <= cap) {

@@ -109,7 +109,7 @@ __device__ __forceinline__ void copy_row(int32_t* dst, const int32_t* __restrict
 // per-order barrier and HBM latencies of one another).
 // MB = 4: 128-thread CTAs at 128 registers, four trajectories per SM (small K).
 template <int NPT, int MB>
-__global__ void __launch_bounds__(MB >= 4 ? 128 : 256, MB) taylor_team_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(MB >= 8 ? 64 : MB >= 4 ? 128 : 256, MB) taylor_team_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Geo g = make_geo(p);
   const Layout L = make_layout(p);
@@ -503,11 +503,13 @@ cudaError_t launch_imad_probe(int blocks, int threads, int iters, long long* out
 
 cudaError_t launch_team_kernel(const Params& p, size_t smem, cudaStream_t stream) {
   const int npt = p.NP <= 1 ? 1 : p.NP <= 2 ? 2 : p.NP <= 4 ? 4 : 8;
-  const bool two = p.team_mb >= 2 && npt <= 2, four = p.team_mb >= 4 && npt <= 2;
-  const void* fn = npt == 1   ? (four ? (const void*)taylor_team_kernel<1, 4>
+  const bool two = p.team_mb >= 2 && npt <= 2, four = p.team_mb >= 4 && npt <= 2, eight = p.team_mb >= 8 && npt <= 2;
+  const void* fn = npt == 1   ? (eight ? (const void*)taylor_team_kernel<1, 8>
+                                 : four ? (const void*)taylor_team_kernel<1, 4>
                                  : two ? (const void*)taylor_team_kernel<1, 2>
                                        : (const void*)taylor_team_kernel<1, 1>)
-                   : npt == 2 ? (four ? (const void*)taylor_team_kernel<2, 4>
+                   : npt == 2 ? (eight ? (const void*)taylor_team_kernel<2, 8>
+                                 : four ? (const void*)taylor_team_kernel<2, 4>
                                  : two ? (const void*)taylor_team_kernel<2, 2>
                                        : (const void*)taylor_team_kernel<2, 1>)
                    : npt == 4 ? (const void*)taylor_team_kernel<4, 1>

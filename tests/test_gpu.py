@@ -112,7 +112,7 @@ def test_ensemble_of_trajectories_bit_exact(gpu):
         assert np.array_equal(r_gpu[:, j], r_cpu), j
 
 
-@pytest.mark.parametrize("mb", ["1", "2", "4"])
+@pytest.mark.parametrize("mb", ["1", "2", "4", "8"])
 @pytest.mark.parametrize("K,N,steps", [(100, 60, 6), (400, 240, 2)])
 def test_team_kernel_two_ctas_per_sm_bit_exact(gpu, monkeypatch, mb, K, N, steps):
     """Ensemble team kernel at one and two resident CTAs per SM (the k-chunk
