@@ -17,9 +17,13 @@ short horizons (tests/test_parity_gpu.py states d per configuration).
 
 from __future__ import annotations
 
+import os
+from collections import OrderedDict
 from dataclasses import dataclass, field
 from decimal import Decimal, localcontext
 from fractions import Fraction
+
+import numpy as np
 
 from .engine import DevicePlan, SystemTables
 from .fixed import FixedFormat
@@ -175,6 +179,35 @@ def _plan_for(system, cfg: StepConfig, ctx: PrecisionContext, reducer, n_traj=1)
     return fmt, DevicePlan(tables, fmt, cfg.order_n, n_traj, device)
 
 
+# Device plans of integrate(), keyed by everything that defines them (the
+# digit tables byte for byte, format, order, device and the kernel-selection
+# environment): repeated calls on one system skip allocation and constant
+# upload. Least-recently-used plans beyond the limit are destroyed.
+_PLAN_CACHE: "OrderedDict[tuple, tuple]" = OrderedDict()
+_PLAN_CACHE_SIZE = 4
+
+
+def _cached_plan(system, cfg: StepConfig, ctx: PrecisionContext, reducer):
+    device, guard = _device_options(reducer)
+    fmt = FixedFormat(ctx.precision_bits, guard)
+    tau = cfg.tau(ctx)
+    tables = SystemTables.build(system, fmt, cfg.order_n, tau.as_fraction())
+    key = (device, guard, ctx.precision_bits, cfg.order_n, tables.dim, tables.c_shift,
+           tuple(os.environ.get(v) for v in ("MPT_KERNEL", "MPT_CLUSTER", "MPT_TEAM_MB")),
+           *(np.ascontiguousarray(a).tobytes() for a in
+             (tables.teq, tables.tj, tables.tk, tables.cst, tables.lin, tables.q, tables.ctab)))
+    hit = _PLAN_CACHE.get(key)
+    if hit is not None:
+        _PLAN_CACHE.move_to_end(key)
+        return hit
+    entry = (fmt, DevicePlan(tables, fmt, cfg.order_n, 1, device))
+    _PLAN_CACHE[key] = entry
+    while len(_PLAN_CACHE) > _PLAN_CACHE_SIZE:
+        _, (_, old) = _PLAN_CACHE.popitem(last=False)
+        old.close()
+    return entry
+
+
 def step(system: QuadraticODESystem, state, cfg: StepConfig, ctx: PrecisionContext, reducer=None) -> tuple:
     """Advance the state by one Taylor step of size cfg.tau (taylor.py:182)."""
     _check_state(system, state)
@@ -215,10 +248,9 @@ def integrate(
     traj.points.append(TrajectoryPoint(step=start_step, state=tuple(state0)))
     if n_steps == start_step:
         return traj
-    fmt, plan = _plan_for(system, cfg, ctx, reducer)
+    fmt, plan = _cached_plan(system, cfg, ctx, reducer)
     dev_stride = 1 if observer is not None else record_stride
-    with plan:
-        steps, recs, status = plan.integrate(fmt.to_digits(state0), n_steps, start_step, dev_stride)
+    steps, recs, status = plan.integrate(fmt.to_digits(state0), n_steps, start_step, dev_stride)
     if status.any():
         raise RangeError("state left the device fixed-point range (|x| >= 2^27) during integrate")
     prec = ctx.precision_bits
