@@ -83,18 +83,27 @@ def check_traj(name, traj, oracle_rows):
             assert same(a, b), f"{name}: oracle differs from reference at step {s}"
 
 
-def integrate_case(name, bits, order, tau, n_steps, stride, init=INIT, system_name="lorenz"):
+def integrate_case(name, bits, order, tau, n_steps, stride, init=INIT, system_name="lorenz",
+                   chunks=None, threshold=None):
+    """chunks/threshold: a non-default ReducePlan (reduction.py:40), passed to
+    the reference as SerialReducer(plan) and to the oracle as its chunk plan."""
     t0 = time.time()
     ctx = M.PrecisionContext(bits)
     system = M.builtin_system(system_name, ctx)
     state0 = tuple(M.mp_from_decimal(t, ctx) for t in init)
     cfg = M.StepConfig(tau_text=tau, order_n=order)
-    traj = M.integrate(system, state0, cfg, n_steps, ctx, record_stride=stride)
+    plan_kw = {}
+    reducer = None
+    if chunks is not None or threshold is not None:
+        plan = M.ReducePlan(num_chunks=chunks or 64, serial_threshold=threshold or 256)
+        reducer = M.SerialReducer(plan)
+        plan_kw = {"chunks": plan.num_chunks, "threshold": plan.serial_threshold}
+    traj = M.integrate(system, state0, cfg, n_steps, ctx, reducer=reducer, record_stride=stride)
     t_ref = time.time() - t0
     t0 = time.time()
     rows = R.integrate(
         sys_to_oracle(system), [dy(v) for v in state0], dy(cfg.tau(ctx)), order, n_steps, bits,
-        stride=stride,
+        stride=stride, **plan_kw,
     )
     t_orc = time.time() - t0
     check_traj(name, traj, rows)
@@ -110,6 +119,7 @@ def integrate_case(name, bits, order, tau, n_steps, stride, init=INIT, system_na
         "init_values": [hx(v) for v in state0],
         "n_steps": n_steps,
         "stride": stride,
+        **({"plan": plan_kw} if plan_kw else {}),
         "system": sys_to_json(system),
         "records": [{"step": p.step, "state": [hx(v) for v in p.state]} for p in traj.points],
     }
@@ -196,6 +206,11 @@ def main():
     cases.append(integrate_case("zero_state_256_n8", 256, 8, "0.01", 5, 1, init=("0", "0", "0")))
     # negative step (forward-backward, test_taylor.py:270)
     cases.append(integrate_case("backward_256_n30", 256, 30, "-0.01", 50, 10))
+    # the chunked branch of the reference reduction (reduction.py:136-146):
+    # orders with i + 1 >= 256 round per chunk of the default 64-chunk plan
+    cases.append(integrate_case("chunked_256_n300_3steps", 256, 300, "0.01", 3, 1))
+    # the plan the timed reference arm runs (serial threshold 32, 64 chunks)
+    cases.append(integrate_case("plan_t32_k500_n200_2steps", k500, 200, "0.01", 2, 1, threshold=32))
     out = os.path.join(HERE, "reference_golden.json")
     with open(out, "w") as fh:
         json.dump({"generator": "tests/golden/make_golden.py", "mpfr": R.mpfr_version(),

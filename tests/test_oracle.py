@@ -34,13 +34,19 @@ def _same(a: R.Dy, hexval: str) -> bool:
 
 @pytest.mark.parametrize(
     "name", ["config0_k50_n40", "cns_pair_128_n20", "config1_k500_n200_3steps", "zero_state_256_n8",
-             "backward_256_n30"]
+             "backward_256_n30",
+             # N = 300 >= the serial threshold 256: the chunked branch of the
+             # reference reduction (reduction.py:136-146) is pinned here
+             "chunked_256_n300_3steps",
+             # the reduction plan the timed reference arm runs (threshold 32)
+             "plan_t32_k500_n200_2steps"]
 )
 def test_oracle_integrate_bit_identical_to_reference(golden, name):
     c = golden[name]
     P = c["prec_bits"]
+    plan = c.get("plan", {})
     rows = R.integrate(_sys(c), [R.dy_from_hex(h) for h in c["init_values"]], R.dy_from_hex(c["tau_value"]),
-                       c["order"], c["n_steps"], P, stride=c["stride"])
+                       c["order"], c["n_steps"], P, stride=c["stride"], **plan)
     assert [s for s, _ in rows] == [r["step"] for r in c["records"]]
     for (s, state), rec in zip(rows, c["records"]):
         for v, h in zip(state, rec["state"]):
