@@ -446,7 +446,184 @@ static int jet_mx(const model_t *M, int32_t *coef) {
   return rc;
 }
 
-static int jet_any(const model_t *M, int32_t *coef) { return M->variant == 1 ? jet_mx(M, coef) : jet(M, coef); }
+/* ---------------------------------------------------------------------------
+ * Value-exact recurrence (variant 2; paper_1908_09301_b200/csrc/taylor_lx.cu).
+ *
+ * The matrix form of variant 1, but every rounding is a function of the VALUE
+ * of an exact column sum only, so the device may partition, fold and sum its
+ * partial products in any order and still agree bit for bit:
+ *
+ *   sd(R)  = the signed-digit recoding of the two's-complement radix-B digits
+ *            r_j of R:  e_j = r_j - B t_j + t_{j-1},  t_j = [r_j >= B/2]
+ *            (digits in [-B/2, B/2]; unique for a value)
+ *   rndb(V) = sd( floor((V + B^2/2) / B^2) ),  V = sum_c col[c] B^c exact
+ *
+ * Per step (a~_0 = the state, canonical digits):
+ *   SB^j     = sd(a~_0^j),  Cb_i = sd(C_i)
+ *   S^{m,j}  = sd( linN[m][j] + sum_{t in m, j_t = j} q_t SB^{k_t} + sum_{t in m, k_t = j} q_t SB^{j_t} )
+ *              (linN = the linear coefficients that are not small integers)
+ *   U_0^m    = rndb( cst_m B^2 + sum_j tprod(lin[m][j], SB^j) + sum_t q_t tprod(SB^{j_t}, SB^{k_t}) )
+ *   order i: X^j      = tprod(U_i^j, Cb_i, Lf+sc-2)                        (exact columns)
+ *            a~^m_{i+1} = rndb(X^m)
+ *            K^{m,j}  = rndb_{W+1}( tprod(S^{m,j}, Cb_i, Lf-2) )           (same scale as C)
+ *            U_{i+1}^m = rndb( sum_j linI[m][j] X^j + sum_{S^{m,j} structural} tprod(U_i^j, K^{m,j}, Lf+sc-2)
+ *                               + sum_{t in m} q_t [ lag_t(i+1) + L'_t(i+1) ] )
+ *            lag_t(2) = tprod(a~^a_1, a~^b_1);  lag_t(j>=3) = tprod(a~^a_{j-1}, a~^b_1) + tprod(a~^a_1, a~^b_{j-1})
+ *            L'_t(j)  = sum_{k=2}^{j-2} tprod(a~^a_{j-k}, a~^b_k)
+ * (tprod without a T argument: T = Lf-2.) linI = the small-integer linear
+ * coefficients; they multiply the exact X columns. Requires small-integer
+ * bilinear coefficients.
+ */
+
+/* digits of R = floor((V + [half] B^drop/2) / B^drop), V = sum col[c] B^c, in
+   the sd recoding, Wout digits; returns 1 when R does not fit Wout sd digits */
+static int sd_cols(const i128 *col, int ncols, int drop, int half, int Wout, int32_t *out) {
+  const int n = (ncols > Wout + drop ? ncols : Wout + drop) + 6;
+  int64_t r[4096 + 32];
+  i128 carry = 0;
+  for (int c = 0; c < n; c++) {
+    i128 v = carry + (c < ncols ? col[c] : 0);
+    if (half && drop > 0 && c == drop - 1) v += RADIX / 2;
+    i128 d = v & (RADIX - 1);
+    carry = (v - d) >> RADIX_BITS;
+    r[c] = (int64_t)d;
+  }
+  if (carry != 0 && carry != -1) return 1;
+  const int nr = n - drop;
+  int t_prev = 0, ovf = 0;
+  for (int j = 0; j < nr; j++) {
+    const int64_t rj = r[j + drop];
+    const int t = rj >= RADIX / 2;
+    const int64_t e = rj - (t ? RADIX : 0) + t_prev;
+    t_prev = t;
+    if (j < Wout) out[j] = (int32_t)e;
+    else if (e != 0) ovf = 1;
+  }
+  /* past digit n the digits are the sign extension: 0 (carry 0) or B-1 (carry -1) */
+  if ((carry == 0 && t_prev != 0) || (carry == -1 && t_prev != 1)) ovf = 1;
+  return ovf;
+}
+
+static int rndb(const i128 *col, int ncols, int Wout, int32_t *out) { return sd_cols(col, ncols, 2, 1, Wout, out); }
+
+static int jet_lx(const model_t *M, int32_t *coef) {
+  int Lf = M->Lf, L = Lf + 1, Wd = W(M), D = M->D, N = M->order, sc = M->sc;
+  int ncols = Lf + 4, KW = Wd + 1;
+  int64_t qint[64], linI[64];
+  int linS[64];
+  for (int t = 0; t < M->NT; t++)
+    if (!small_int(M->q + (size_t)t * Wd, Lf, &qint[t])) return -5;
+  for (int e = 0; e < D * D; e++) {
+    linS[e] = small_int(M->lin + (size_t)e * Wd, Lf, &linI[e]);
+    if (!linS[e]) linI[e] = 0;
+  }
+  i128 *col = malloc(sizeof(i128) * (size_t)(ncols + 8));
+  i128 *X = malloc(sizeof(i128) * (size_t)D * (ncols + 8));
+  int32_t *SB = malloc(sizeof(int32_t) * (size_t)D * Wd);
+  int32_t *S = calloc((size_t)D * D * Wd, sizeof(int32_t));
+  int32_t *K = malloc(sizeof(int32_t) * (size_t)D * D * KW);
+  int32_t *Cb = malloc(sizeof(int32_t) * (size_t)(N > 0 ? N : 1) * Wd);
+  int32_t *U = malloc(sizeof(int32_t) * (size_t)D * Wd);
+  int32_t *U2 = malloc(sizeof(int32_t) * (size_t)D * Wd);
+  int snz[256];
+  i128 acc[4096 + 8];
+  int rc = 0;
+#define CO(m, i) (coef + ((size_t)(m) * (N + 1) + (i)) * Wd)
+  for (int m = 0; m < D && !rc; m++) {
+    for (int d = 0; d <= Lf; d++) acc[d] = CO(m, 0)[d];
+    if (sd_cols(acc, Wd, 0, 0, Wd, SB + (size_t)m * Wd)) rc = 1;
+  }
+  for (int i = 0; i < N && !rc; i++) {
+    for (int d = 0; d <= Lf; d++) acc[d] = M->ctab[(size_t)i * Wd + d];
+    if (sd_cols(acc, Wd, 0, 0, Wd, Cb + (size_t)i * Wd)) rc = 1;
+  }
+  for (int m = 0; m < D && !rc; m++)
+    for (int j = 0; j < D && !rc; j++) {
+      int any = !linS[m * D + j];
+      for (int d = 0; d <= Lf; d++) acc[d] = linS[m * D + j] ? 0 : M->lin[((size_t)m * D + j) * Wd + d];
+      for (int t = 0; t < M->NT; t++) {
+        if (M->teq[t] != m) continue;
+        if (M->tj[t] == j) {
+          any = 1;
+          for (int d = 0; d <= Lf; d++) acc[d] += (i128)qint[t] * SB[(size_t)M->tk[t] * Wd + d];
+        }
+        if (M->tk[t] == j) {
+          any = 1;
+          for (int d = 0; d <= Lf; d++) acc[d] += (i128)qint[t] * SB[(size_t)M->tj[t] * Wd + d];
+        }
+      }
+      snz[m * D + j] = any;
+      if (sd_cols(acc, Wd, 0, 0, Wd, S + ((size_t)m * D + j) * Wd)) rc = 1;
+    }
+  for (int m = 0; m < D && !rc; m++) {
+    memset(col, 0, sizeof(i128) * ncols);
+    for (int j = 0; j <= Lf; j++) col[2 + j] += (i128)M->cst[(size_t)m * Wd + j];
+    for (int j = 0; j < D; j++) tprod_acc(M->lin + ((size_t)m * D + j) * Wd, SB + (size_t)j * Wd, L, Lf - 2, col, ncols);
+    for (int t = 0; t < M->NT; t++) {
+      if (M->teq[t] != m) continue;
+      memset(acc, 0, sizeof(i128) * ncols);
+      tprod_acc(SB + (size_t)M->tj[t] * Wd, SB + (size_t)M->tk[t] * Wd, L, Lf - 2, acc, ncols);
+      for (int c = 0; c < ncols; c++) col[c] += (i128)qint[t] * acc[c];
+    }
+    if (rndb(col, ncols, Wd, U + (size_t)m * Wd)) rc = 1;
+  }
+  for (int i = 0; i < N && !rc; i++) {
+    const int32_t *C = Cb + (size_t)i * Wd;
+    for (int m = 0; m < D; m++) {
+      i128 *x = X + (size_t)m * (ncols + 8);
+      memset(x, 0, sizeof(i128) * ncols);
+      tprod_acc(U + (size_t)m * Wd, C, L, Lf + sc - 2, x, ncols);
+      if (rndb(x, ncols, Wd, CO(m, i + 1))) rc = 1;
+    }
+    if (i + 1 >= N) break;
+    for (int e = 0; e < D * D; e++) {
+      if (!snz[e]) continue;
+      memset(col, 0, sizeof(i128) * ncols);
+      tprod_acc(S + (size_t)e * Wd, C, L, Lf - 2, col, ncols);
+      if (rndb(col, ncols, KW, K + (size_t)e * KW)) rc = 1;
+    }
+    const int j = i + 1;
+    for (int m = 0; m < D; m++) {
+      memset(col, 0, sizeof(i128) * ncols);
+      for (int jj = 0; jj < D; jj++) {
+        if (linI[m * D + jj]) {
+          const i128 *x = X + (size_t)jj * (ncols + 8);
+          for (int c = 0; c < ncols; c++) col[c] += (i128)linI[m * D + jj] * x[c];
+        }
+        if (snz[m * D + jj])
+          tprod_acc2(U + (size_t)jj * Wd, L, K + ((size_t)m * D + jj) * KW, KW, Lf + sc - 2, col, ncols);
+      }
+      for (int t = 0; t < M->NT; t++) {
+        if (M->teq[t] != m) continue;
+        const int a = M->tj[t], b = M->tk[t];
+        memset(acc, 0, sizeof(i128) * ncols);
+        if (j == 2) tprod_acc(CO(a, 1), CO(b, 1), L, Lf - 2, acc, ncols);
+        if (j >= 3) {
+          tprod_acc(CO(a, j - 1), CO(b, 1), L, Lf - 2, acc, ncols);
+          tprod_acc(CO(a, 1), CO(b, j - 1), L, Lf - 2, acc, ncols);
+        }
+        for (int k = 2; k <= j - 2; k++) tprod_acc(CO(a, j - k), CO(b, k), L, Lf - 2, acc, ncols);
+        for (int c = 0; c < ncols; c++) col[c] += (i128)qint[t] * acc[c];
+      }
+      if (rndb(col, ncols, Wd, U2 + (size_t)m * Wd)) rc = 1;
+    }
+    memcpy(U, U2, sizeof(int32_t) * (size_t)D * Wd);
+  }
+#undef CO
+  free(col);
+  free(X);
+  free(SB);
+  free(S);
+  free(K);
+  free(Cb);
+  free(U);
+  free(U2);
+  return rc;
+}
+
+static int jet_any(const model_t *M, int32_t *coef) {
+  return M->variant == 2 ? jet_lx(M, coef) : M->variant == 1 ? jet_mx(M, coef) : jet(M, coef);
+}
 
 /* round the canonical digit vector to `prec` significant bits, ties to even */
 static int round_prec(int32_t *d, int W, int prec) {

@@ -30,7 +30,7 @@ def guard_digits(t: float) -> int:
     return 3 + math.ceil(0.3935 * t)
 
 
-VARIANTS = [0, 1]  # 0: per-order C-product recurrence, 1: matrix recurrence (mx kernel)
+VARIANTS = [0, 1, 2]  # 0: per-order C-product recurrence, 1: matrix recurrence (mx kernel), 2: value-exact (lx kernel)
 
 
 def run_model(case, guard_bits=32, variant=0):
@@ -97,7 +97,7 @@ def test_jets_match_reference_jets(golden, variant):
         k = 7
         tables = SystemTables.build(system, fmt, N, Fraction(1, 1 << k))
         st = fmt.to_digits([frac(h) for h in c["state"]])
-        if variant == 1 and not all(_small_int_q(tables)):
+        if variant >= 1 and not all(_small_int_q(tables)):
             continue
         coef = FX.compute_jet(tables, fmt.frac_digits, N, st, variant=variant)
         for m in range(system.dim):
