@@ -41,6 +41,10 @@ EXPORTS = (
 )
 
 
+# error codes of include/mptaylor_b200.h
+MPT_EINVAL, MPT_ENODEV, MPT_ECUDA, MPT_EUNSUP, MPT_ERANGE = -1, -2, -3, -4, -5
+
+
 class NativeUnavailable(RuntimeError):
     """The CUDA engine cannot run here (library not built or no GPU)."""
 

@@ -15,17 +15,6 @@ namespace mpt {
 size_t smem_bytes(const Params& p);
 cudaError_t launch_team_kernel(const Params& p, size_t smem, cudaStream_t stream);
 cudaError_t launch_imad_probe(int blocks, int threads, int iters, long long* out, cudaStream_t s);
-size_t cluster_smem_bytes(const Params& p, int G);
-cudaError_t launch_cluster_kernel(const Params& p, int G, size_t smem, cudaStream_t stream);
-int max_cluster_size(const Params& p, size_t smem, int want);
-size_t pipe_smem_bytes(const Params& p, int G);
-bool pipe_supported(const Params& p);
-cudaError_t launch_pipe_kernel(const Params& p, int G, size_t smem, cudaStream_t stream);
-int pipe_max_cluster(const Params& p, size_t smem, int want);
-size_t relay_smem_bytes(const Params& p, int G);
-bool relay_supported(const Params& p);
-cudaError_t launch_relay_kernel(const Params& p, int G, size_t smem, cudaStream_t stream);
-int relay_max_cluster(const Params& p, size_t smem, int want);
 bool grid_supported(const Params& p);
 size_t grid_smem_bytes(const Params& p, int kc);
 size_t grid_scratch_bytes(const Params& p);
@@ -67,9 +56,8 @@ struct mpt_plan {
   bool have_constants = false;
   unsigned long long* d_counters = nullptr;
   bool counting = false;
-  int kernel = 0;    // 1 team (rows in HBM/L2), 2 cluster (rows in smem), 3 pipeline, 4 grid (all SMs),
-                     // 5 relay, 6 mx (matrix recurrence)
-  int cluster = 1;   // CTAs per trajectory for the cluster kernel
+  int kernel = 0;    // 1 team (rows in HBM/L2), 4 grid (all SMs), 6 mx (matrix recurrence)
+  int cluster = 1;   // CTAs per trajectory (mx), co-resident CTAs (grid)
   size_t smem_cluster = 0;
   int optin = 0;
   int nsm = 148;     // SMs of the device
@@ -103,8 +91,9 @@ static int setup_grid(mpt_plan* pl) {
   return MPT_OK;
 }
 
-// choose the kernel: the smem-resident cluster kernel when the rows fit,
-// one cluster of `want` CTAs per trajectory (clamped to what co-schedules)
+// choose the kernel (0 = automatic): one trajectory -> mx (cluster of `want` CTAs,
+// clamped to what co-schedules) when the system fits it, else the grid kernel on
+// every SM; ensembles -> team (one CTA per trajectory)
 static int choose_kernel(mpt_plan* pl, int kernel, int want) {
   mpt::Params& p = pl->p;
   pl->requested_kernel = kernel;
@@ -155,26 +144,6 @@ static int choose_kernel(mpt_plan* pl, int kernel, int want) {
     }
     return fail(MPT_EUNSUP, "the mx kernel does not support this system/precision");
   }
-  // the relay kernel (lead CTA + bulk CTAs) needs the constants and G >= 2
-  if ((kernel == 0 || kernel == 5) && pl->have_constants && mpt::relay_supported(p) && (kernel == 5 || p.n_traj == 1)) {
-    for (int G : tries) {
-      if (G > want || G < 2) continue;
-      size_t s = mpt::relay_smem_bytes(p, G);
-      if (s > (size_t)pl->optin) continue;
-      if (mpt::relay_max_cluster(p, s, G) < 1) continue;
-      pl->kernel = 5;
-      pl->cluster = G;
-      pl->smem_cluster = s;
-      return MPT_OK;
-    }
-  }
-  if (kernel == 5) {
-    if (!pl->have_constants) {
-      pl->kernel = 0;
-      return MPT_OK;
-    }
-    return fail(MPT_EUNSUP, "the relay kernel does not support this system/precision (shared memory)");
-  }
   // ensembles that fill every SM: one trajectory per CTA (team kernel, two
   // CTAs per SM) beats a per-trajectory cluster (measured ens100-ens800)
   if (kernel == 0 && p.n_traj >= pl->nsm) {
@@ -182,37 +151,6 @@ static int choose_kernel(mpt_plan* pl, int kernel, int want) {
     pl->cluster = 1;
     return MPT_OK;
   }
-  // the pipelined kernel needs the constants (integer bilinear coefficients)
-  if ((kernel == 0 || kernel == 3) && pl->have_constants && mpt::pipe_supported(p)) {
-    for (int G : tries) {
-      if (G > want) continue;
-      size_t s = mpt::pipe_smem_bytes(p, G);
-      if (s > (size_t)pl->optin) continue;
-      if (G > 1 && mpt::pipe_max_cluster(p, s, G) < 1) continue;
-      pl->kernel = 3;
-      pl->cluster = G;
-      pl->smem_cluster = s;
-      return MPT_OK;
-    }
-  }
-  if (kernel == 3) {
-    if (!pl->have_constants) {  // decided again once the constants are known
-      pl->kernel = 0;
-      return MPT_OK;
-    }
-    return fail(MPT_EUNSUP, "the pipelined kernel does not support this system/precision");
-  }
-  for (int G : tries) {
-    if (G > want) continue;
-    size_t s = mpt::cluster_smem_bytes(p, G);
-    if (s > (size_t)pl->optin) continue;
-    if (G > 1 && mpt::max_cluster_size(p, s, G) < 1) continue;
-    pl->kernel = 2;
-    pl->cluster = G;
-    pl->smem_cluster = s;
-    return MPT_OK;
-  }
-  if (kernel == 2) return fail(MPT_EUNSUP, "coefficient rows do not fit shared memory for the cluster kernel");
   if (kernel == 0 && pl->have_constants && mpt::grid_supported(p) && setup_grid(pl) == MPT_OK) {
     pl->kernel = 4;
     pl->cluster = pl->grid_blocks;
@@ -239,8 +177,10 @@ int mpt_device_count(void) {
 
 int mpt_record_count(int n_steps, int start_step, int stride) {
   if (stride < 1 || n_steps < start_step) return MPT_EINVAL;
+  // records: start_step, every multiple of stride in (start_step, n_steps], and
+  // n_steps itself when it is not one of them (taylor.py:202 integrate)
   int n = 1 + (n_steps / stride - start_step / stride);
-  if (n_steps % stride) n += 1;
+  if (n_steps % stride && n_steps > start_step) n += 1;
   return n;
 }
 
@@ -361,6 +301,15 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
     }
   }
   pl->smem = smem;
+  {
+    // team kernel, Cauchy phase: one thread per (pair, balanced window pair) unit
+    // (taylor_kernel.cu phase A); more units than threads would be left out
+    const int ngb = (2 * p.Lf) / mpt::kR - (p.Lf - 2) / mpt::kR + 1;
+    if (p.NP * ((ngb + 1) / 2) > p.nthreads) {
+      delete pl;
+      return fail(MPT_EUNSUP, "too many product pairs for this precision on the device (pairs x column windows > threads)");
+    }
+  }
   size_t rows = (size_t)n_traj * dim * (order + 1);
 #define ALLOC(ptr, bytes)                                                         \
   do {                                                                            \
@@ -393,13 +342,10 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
   {
     const char* ek = getenv("MPT_KERNEL");
     const char* ec = getenv("MPT_CLUSTER");
-    int kernel = ek ? (strcmp(ek, "team") == 0      ? 1
-                       : strcmp(ek, "cluster") == 0 ? 2
-                       : strcmp(ek, "pipe") == 0    ? 3
-                       : strcmp(ek, "grid") == 0    ? 4
-                       : strcmp(ek, "relay") == 0   ? 5
-                       : strcmp(ek, "mx") == 0      ? 6
-                                                    : 0)
+    int kernel = ek ? (strcmp(ek, "team") == 0   ? 1
+                       : strcmp(ek, "grid") == 0 ? 4
+                       : strcmp(ek, "mx") == 0   ? 6
+                                                 : 0)
                     : 0;
     int want = ec ? atoi(ec) : (n_traj == 1 ? 16 : 1);
     int rc = choose_kernel(pl, kernel, want < 1 ? 1 : want);
@@ -413,7 +359,8 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
 }
 
 int mpt_plan_configure(mpt_plan* pl, int kernel, int cluster) {
-  if (!pl || kernel < 0 || kernel > 6 || cluster < 1 || cluster > 16) return fail(MPT_EINVAL, "bad configuration");
+  if (!pl || (kernel != 0 && kernel != 1 && kernel != 4 && kernel != 6) || cluster < 1 || cluster > 16)
+    return fail(MPT_EINVAL, "bad configuration");
   return choose_kernel(pl, kernel, cluster);
 }
 
@@ -552,14 +499,9 @@ static int launch(mpt_plan* pl, int n_steps, int start_step, int stride, cudaStr
     CK(cudaMemsetAsync(pl->d_status, 0, sizeof(int32_t) * p.n_traj, stream));
     p.gscratch = pl->d_mxscratch;
     CK(mpt::launch_mx_kernel(p, pl->cluster, pl->smem_cluster, stream));
-  } else if (pl->kernel == 5)
-    CK(mpt::launch_relay_kernel(p, pl->cluster, pl->smem_cluster, stream));
-  else if (pl->kernel == 3)
-    CK(mpt::launch_pipe_kernel(p, pl->cluster, pl->smem_cluster, stream));
-  else if (pl->kernel == 2)
-    CK(mpt::launch_cluster_kernel(p, pl->cluster, pl->smem_cluster, stream));
-  else
+  } else {
     CK(mpt::launch_team_kernel(p, pl->smem, stream));
+  }
   CK(cudaEventRecord(pl->ev1, stream));
   return MPT_OK;
 }

@@ -52,6 +52,9 @@ class SystemTables:
         )
 
 
+KERNEL_NAMES = {1: "team", 4: "grid", 6: "mx"}  # include/mptaylor_b200.h mpt_plan_configure
+
+
 def _p(a: np.ndarray):
     return a.ctypes.data_as(_native.i32p)
 
@@ -107,7 +110,7 @@ class DevicePlan:
         kern, cl = ctypes.c_int32(), ctypes.c_int32()
         _native.check(self.lib.mpt_plan_kernel(self.h, ctypes.byref(kern), ctypes.byref(cl)))
         return {"smem_bytes": s.value, "k_chunk": k.value, "threads": t.value,
-                "kernel": {1: "team", 2: "cluster", 3: "pipe", 4: "grid", 5: "relay", 6: "mx"}.get(kern.value, "?"), "cluster": cl.value}
+                "kernel": KERNEL_NAMES.get(kern.value, "?"), "cluster": cl.value}
 
     @property
     def variant(self) -> int:
@@ -129,7 +132,7 @@ class DevicePlan:
         return {"variant": 0}
 
     def configure(self, kernel: str = "auto", cluster: int = 8):
-        code = {"auto": 0, "team": 1, "cluster": 2, "pipe": 3, "grid": 4, "relay": 5, "mx": 6}[kernel]
+        code = {"auto": 0, **{v: k for k, v in KERNEL_NAMES.items()}}[kernel]
         _native.check(self.lib.mpt_plan_configure(self.h, code, cluster))
 
     def _state(self, state: np.ndarray) -> np.ndarray:

@@ -26,10 +26,10 @@ import numpy as np
 
 from .cns import AGREEMENT_EXACT, tc_from_series
 from .engine import DevicePlan, SystemTables
-from .fixed import FixedFormat
-from .mp import PrecisionContext, bits_for_digits, mp_from_decimal
+from .fixed import MAX_INT_BITS, FixedFormat
+from .mp import _DECIMAL_RE, PrecisionContext, RangeError, _round_scaled, bits_for_digits, mp_from_decimal
 from .systems import builtin_system
-from .taylor import exact_time
+from .taylor import checked_out_plan, exact_time
 
 CANON_INIT = ("-15.8", "-17.48", "35.64")
 EXACT_CODE = 1 << 30  # AGREEMENT_EXACT in integer matrices
@@ -81,18 +81,55 @@ class EnsembleRun:
         return [flat[i * d:(i + 1) * d] for i in range(r.shape[0])]
 
 
+def decimal_to_fixed_int(text: str, bits: int, fmt: FixedFormat) -> int:
+    """fmt.to_int(mp_from_decimal(text, ctx)) on plain integers: the decimal is
+    rounded to `bits` significant bits (ties to even, mp.py:122) and then placed
+    on the fixed-point grid; no MPValue / Fraction objects (ensemble uploads
+    convert 3 M values per call)."""
+    stripped = text.strip()
+    if not _DECIMAL_RE.match(stripped):
+        raise ValueError(f"not a valid decimal literal: {text!r}")
+    neg = stripped[0] == "-"
+    mant_txt, _, exp_txt = stripped.lstrip("+-").replace("E", "e").partition("e")
+    whole, _, frac = mant_txt.partition(".")
+    digits = int((whole or "0") + frac)
+    e10 = (int(exp_txt) if exp_txt else 0) - len(frac)
+    if digits == 0:
+        return 0
+    if abs(len(str(digits)) + e10) > 10**6:
+        raise RangeError(f"decimal exponent out of range: {text!r}")
+    num, den = (digits * 10**e10, 1) if e10 >= 0 else (digits, 10**(-e10))
+    mant, exp = _round_scaled(1, num, den, bits)
+    sh = exp + fmt.frac_bits
+    if sh >= 0:
+        x = mant << sh
+    else:
+        q, r = divmod(mant, 1 << -sh)
+        half = 1 << (-sh - 1)
+        x = q + (1 if r > half or (r == half and q & 1) else 0)
+    if x >> (fmt.frac_bits + MAX_INT_BITS):
+        raise RangeError(f"|value| >= 2^{MAX_INT_BITS} does not fit the device format")
+    return -x if neg else x
+
+
+def states_from_decimals(inits, bits: int, fmt: FixedFormat) -> np.ndarray:
+    """[members, dim, W] digit rows of decimal initial conditions parsed at `bits`."""
+    dim = len(inits[0])
+    flat = [decimal_to_fixed_int(t, bits, fmt) for row in inits for t in row]
+    return fmt.ints_to_digits(flat).reshape(len(inits), dim, fmt.width)
+
+
 def run_members(system_name: str, inits, bits: int, order: int, tau_text: str, n_steps: int, stride: int,
                 device: int = 0, kernel: str = "auto") -> EnsembleRun:
-    """Integrate every member of `inits` (decimal texts, parsed at `bits`) on one GPU."""
+    """Integrate every member of `inits` (decimal texts, parsed at `bits`) on one GPU.
+    The device plan (buffers, constant tables) is cached across calls."""
     ctx = PrecisionContext(bits)
     system = builtin_system(system_name, ctx) if isinstance(system_name, str) else system_name(ctx)
-    fmt = FixedFormat(bits)
     tau = mp_from_decimal(tau_text, ctx)
-    tables = SystemTables.build(system, fmt, order, tau.as_fraction())
-    states = np.stack([fmt.to_digits([mp_from_decimal(t, ctx) for t in row]) for row in inits])
-    with DevicePlan(tables, fmt, order, len(inits), device) as plan:
-        if kernel != "auto":
-            plan.configure(kernel, 1)
+    fmt = FixedFormat(bits)
+    states = states_from_decimals(inits, bits, fmt)
+    with checked_out_plan(system, order, tau.as_fraction(), ctx, None, n_traj=len(inits), device=device) as (_, plan):
+        plan.configure(kernel, 16 if len(inits) == 1 else 1)
         steps, recs, status = plan.integrate(states, n_steps, 0, stride)
         ms = plan.last_kernel_ms()
     return EnsembleRun(bits, order, tau_text, fmt, steps, recs, status, ms)
@@ -149,6 +186,16 @@ def divergence_times(steps, tau_text: str, agreement: np.ndarray, d: int) -> lis
     return out
 
 
+def tc_steps(steps, agreement_by_member: np.ndarray, d: int) -> np.ndarray:
+    """divergence_times as step indices, vectorised: [members] step of the last
+    sample before the first one with fewer than d digits (the last sample when
+    none fails, 0 when the first one fails); t_c = step * tau exactly."""
+    steps = np.asarray(steps, np.int64)
+    fails = np.asarray(agreement_by_member) < d
+    first = np.where(fails.any(axis=1), fails.argmax(axis=1), len(steps))
+    return np.where(first == 0, 0, steps[np.maximum(first, 1) - 1]).astype(np.int64)
+
+
 @dataclass
 class EnsembleReport:
     base: tuple  # (bits, order)
@@ -180,6 +227,89 @@ def ensemble_tc(inits, K: int, N: int, tau_text: str, t_end_text: str, d: int = 
     return EnsembleReport((bb, N), (vb, N + verify_margin[1]), tau_text, base.steps, agr,
                           divergence_times(base.steps, tau_text, agr, d), base.records[-1],
                           {"base": base.kernel_ms, "verify": ver.kernel_ms})
+
+
+# ------------------------------------------------------------------ T_c-K sweep
+@dataclass
+class SweepReport:
+    """One (K, N) point of the T_c-K diagram over the whole ensemble (every rank
+    holds the gathered arrays; member order = perturbed_inits order)."""
+
+    K: int
+    N: int
+    base: tuple  # (bits, order)
+    verify: tuple
+    tau_text: str
+    steps: np.ndarray  # [nrec] sampled step indices
+    agreement: np.ndarray  # [members, nrec] digits (EXACT_CODE = identical)
+    tc_step: np.ndarray  # [members] step index of t_c (t_c = tc_step * tau, exact)
+    final_xyz: np.ndarray  # [members, dim] float64 view of the base run's final state
+    final_digits: np.ndarray  # [members, dim, W_base] its exact digits
+    world: int = 1
+    kernel_ms: dict = field(default_factory=dict)
+
+    def t_c(self) -> list:
+        return [exact_time(int(s), self.tau_text) for s in self.tc_step]
+
+    def tc_mean(self) -> float:
+        return float(np.mean([float(t) for t in self.t_c()]))
+
+
+def _device_run_fn(system_name, device):
+    def run(inits, bits, order, tau_text, n_steps, stride):
+        return run_members(system_name, inits, bits, order, tau_text, n_steps, stride, device)
+
+    return run
+
+
+def tc_sweep(K: int, N: int, n_members: int, n_steps: int, rank: int = 0, world: int = 1, device: int = 0,
+             tau_text: str = "0.01", d: int = 10, stride: int = 100, seed: int = 0, amplitude: str = "1e-20",
+             verify_margin=(50, 30), system_name: str = "lorenz", run_fn=None, gather: bool = True,
+             gather_device=None) -> SweepReport:
+    """BASELINE configs[4] at one (K, N): this rank's shard of the M seeded members
+    is integrated at (K, N) and at the verify budget (K+50, N+30) on `device`, each
+    member's divergence time t_c is taken against its own verify run (reference
+    cns.py:202 estimate_tc / :254 cns_run semantics, as scripts/tc_sweep.py does
+    per sweep point through cns.py:290 tc_diagram), and x, y, z and t_c of all M
+    members are all-gathered (torch.distributed; NCCL when `gather_device` is a
+    CUDA device, gloo on CPU). No collective touches the integration itself.
+
+    run_fn(inits, bits, order, tau_text, n_steps, stride) -> EnsembleRun replaces
+    the device run in the host-logic tests."""
+    if n_steps % stride:
+        raise ValueError(f"n_steps {n_steps} is not a multiple of the sampling stride {stride}")
+    lo, hi = shard_bounds(n_members, world, rank)
+    inits = perturbed_inits(n_members, seed=seed, amplitude=amplitude)[lo:hi]
+    run = run_fn or _device_run_fn(system_name, device)
+    bb, vb = bits_for_digits(K), bits_for_digits(K + verify_margin[0])
+    vn = N + verify_margin[1]
+    if hi > lo:
+        base = run(inits, bb, N, tau_text, n_steps, stride)
+        ver = run(inits, vb, vn, tau_text, n_steps, stride)
+        if base.status.any() or ver.status.any():
+            raise ArithmeticError("a member left the device fixed-point range")
+        steps = np.asarray(base.steps, np.int64)
+        agr = agreement_matrix(base, ver).T.copy()  # [members, nrec]
+        tc_step = tc_steps(steps, agr, d)
+        final_digits = np.ascontiguousarray(base.records[-1])
+        scale = 2.0 ** (-base.fmt.frac_bits)
+        final_xyz = np.array([[x * scale for x in row] for row in base.ints(base.records.shape[0] - 1)], np.float64)
+        kms = {"base": base.kernel_ms, "verify": ver.kernel_ms}
+    else:  # more ranks than members: an empty shard still takes part in the gather
+        fmt = FixedFormat(bb)
+        nrec = n_steps // stride + 1
+        steps = np.arange(nrec, dtype=np.int64) * stride
+        agr = np.zeros((0, nrec), np.int64)
+        tc_step = np.zeros(0, np.int64)
+        final_digits = np.zeros((0, len(CANON_INIT), fmt.width), np.int32)
+        final_xyz = np.zeros((0, len(CANON_INIT)), np.float64)
+        kms = {"base": 0.0, "verify": 0.0}
+    if gather and world > 1:
+        agr = gather_rows(agr, n_members, world, rank, gather_device)
+        tc_step = gather_rows(tc_step, n_members, world, rank, gather_device)
+        final_digits = gather_rows(final_digits, n_members, world, rank, gather_device)
+        final_xyz = gather_rows(final_xyz, n_members, world, rank, gather_device)
+    return SweepReport(K, N, (bb, N), (vb, vn), tau_text, steps, agr, tc_step, final_xyz, final_digits, world, kms)
 
 
 # ------------------------------------------------------------------ gather

@@ -12,19 +12,22 @@ What changes underneath:
     context precision P (round-to-nearest-even) after every step, so every
     recorded state is a P-bit MPValue like the reference's.
 Results agree with the reference to a relative tolerance of 10^-(K-d) over
-short horizons (tests/test_parity_gpu.py states d per configuration).
+short horizons (tests/test_gpu.py states the guard digits d(t) per run).
 """
 
 from __future__ import annotations
 
 import os
+import threading
 from collections import OrderedDict
+from contextlib import contextmanager
 from dataclasses import dataclass, field
 from decimal import Decimal, localcontext
 from fractions import Fraction
 
 import numpy as np
 
+from ._native import MPT_ERANGE, NativeError
 from .engine import DevicePlan, SystemTables
 from .fixed import FixedFormat
 from .mp import MPValue, PrecisionContext, RangeError, mp_from_decimal
@@ -135,13 +138,11 @@ def compute_jet(system: QuadraticODESystem, state, order_n: int, ctx: PrecisionC
     st = fmt.to_digits(state)
     last = None
     for k in (7, 10, 14, 20, 28):
-        scale = Fraction(1, 1 << k)
-        tables = SystemTables.build(system, fmt, order_n, scale)
         try:
-            with DevicePlan(tables, fmt, order_n, 1, device) as plan:
+            with checked_out_plan(system, order_n, Fraction(1, 1 << k), ctx, reducer) as (_, plan):
                 coef = plan.compute_jet(st)[0]
-        except Exception as exc:  # range exceeded: retry with a smaller scale
-            if "range" in str(exc):
+        except NativeError as exc:
+            if exc.code == MPT_ERANGE:  # a coefficient left the range: retry with a smaller scale
                 last = exc
                 continue
             raise
@@ -171,48 +172,94 @@ def horner_eval(jet_row, tau: MPValue, ctx: PrecisionContext) -> MPValue:
     return acc
 
 
-def _plan_for(system, cfg: StepConfig, ctx: PrecisionContext, reducer, n_traj=1):
-    device, guard = _device_options(reducer)
+# Device plans of integrate() / step() / compute_jet(), keyed by everything
+# that defines them (the digit tables byte for byte, format, order, device, the
+# kernel-selection environment and the process id): repeated calls on one
+# system skip allocation and constant upload. A plan owns one set of device
+# buffers, so an entry is used by one caller at a time (per-entry lock; other
+# keys run concurrently, as the reference's reentrant integrate() does).
+# Least-recently-used entries beyond the limit are destroyed once idle.
+_PLAN_CACHE: "OrderedDict[tuple, _PlanEntry]" = OrderedDict()
+_PLAN_CACHE_SIZE = 8
+_PLAN_CACHE_LOCK = threading.Lock()
+
+
+class _PlanEntry:
+    def __init__(self, fmt, plan):
+        self.fmt, self.plan = fmt, plan
+        self.lock = threading.Lock()
+        self.users = 0
+        self.evicted = False
+
+
+def _forget_plans_in_child():
+    # a forked child inherits handles of the parent's CUDA context: never free them there
+    for entry in _PLAN_CACHE.values():
+        entry.plan.h = None
+    _PLAN_CACHE.clear()
+
+
+os.register_at_fork(after_in_child=_forget_plans_in_child)
+
+
+def _plan_key(tables: SystemTables, guard: int, prec_bits: int, order: int, device: int, n_traj: int) -> tuple:
+    return (os.getpid(), device, n_traj, guard, prec_bits, order, tables.dim, tables.c_shift,
+            tuple(os.environ.get(v) for v in ("MPT_KERNEL", "MPT_CLUSTER", "MPT_TEAM_MB")),
+            *(np.ascontiguousarray(a).tobytes() for a in
+              (tables.teq, tables.tj, tables.tk, tables.cst, tables.lin, tables.q, tables.ctab)))
+
+
+@contextmanager
+def checked_out_plan(system, order_n: int, scale: Fraction, ctx: PrecisionContext, reducer, n_traj: int = 1,
+                     device=None):
+    """(fmt, plan) of n_traj trajectories for (system, order, step scale),
+    exclusively held for the duration of the with-block."""
+    dev, guard = _device_options(reducer)
+    device = dev if device is None else device
     fmt = FixedFormat(ctx.precision_bits, guard)
-    tau = cfg.tau(ctx)
-    tables = SystemTables.build(system, fmt, cfg.order_n, tau.as_fraction())
-    return fmt, DevicePlan(tables, fmt, cfg.order_n, n_traj, device)
-
-
-# Device plans of integrate(), keyed by everything that defines them (the
-# digit tables byte for byte, format, order, device and the kernel-selection
-# environment): repeated calls on one system skip allocation and constant
-# upload. Least-recently-used plans beyond the limit are destroyed.
-_PLAN_CACHE: "OrderedDict[tuple, tuple]" = OrderedDict()
-_PLAN_CACHE_SIZE = 4
-
-
-def _cached_plan(system, cfg: StepConfig, ctx: PrecisionContext, reducer):
-    device, guard = _device_options(reducer)
-    fmt = FixedFormat(ctx.precision_bits, guard)
-    tau = cfg.tau(ctx)
-    tables = SystemTables.build(system, fmt, cfg.order_n, tau.as_fraction())
-    key = (device, guard, ctx.precision_bits, cfg.order_n, tables.dim, tables.c_shift,
-           tuple(os.environ.get(v) for v in ("MPT_KERNEL", "MPT_CLUSTER", "MPT_TEAM_MB")),
-           *(np.ascontiguousarray(a).tobytes() for a in
-             (tables.teq, tables.tj, tables.tk, tables.cst, tables.lin, tables.q, tables.ctab)))
-    hit = _PLAN_CACHE.get(key)
-    if hit is not None:
+    tables = SystemTables.build(system, fmt, order_n, scale)
+    key = _plan_key(tables, guard, ctx.precision_bits, order_n, device, n_traj)
+    stale = []
+    with _PLAN_CACHE_LOCK:
+        entry = _PLAN_CACHE.get(key)
+        if entry is None:
+            entry = _PLAN_CACHE[key] = _PlanEntry(fmt, DevicePlan(tables, fmt, order_n, n_traj, device))
         _PLAN_CACHE.move_to_end(key)
-        return hit
-    entry = (fmt, DevicePlan(tables, fmt, cfg.order_n, 1, device))
-    _PLAN_CACHE[key] = entry
-    while len(_PLAN_CACHE) > _PLAN_CACHE_SIZE:
-        _, (_, old) = _PLAN_CACHE.popitem(last=False)
-        old.close()
-    return entry
+        entry.users += 1
+        while len(_PLAN_CACHE) > _PLAN_CACHE_SIZE:
+            _, old = _PLAN_CACHE.popitem(last=False)
+            old.evicted = True
+            if old.users == 0:
+                stale.append(old)
+    for old in stale:
+        old.plan.close()
+    try:
+        with entry.lock:
+            yield entry.fmt, entry.plan
+    finally:
+        with _PLAN_CACHE_LOCK:
+            entry.users -= 1
+            close_now = entry.evicted and entry.users == 0
+        if close_now:
+            entry.plan.close()
+
+
+def clear_plan_cache() -> None:
+    """Destroy every idle cached device plan (tests; before a device reset)."""
+    with _PLAN_CACHE_LOCK:
+        entries = list(_PLAN_CACHE.values())
+        _PLAN_CACHE.clear()
+        for e in entries:
+            e.evicted = True
+        idle = [e for e in entries if e.users == 0]
+    for e in idle:
+        e.plan.close()
 
 
 def step(system: QuadraticODESystem, state, cfg: StepConfig, ctx: PrecisionContext, reducer=None) -> tuple:
     """Advance the state by one Taylor step of size cfg.tau (taylor.py:182)."""
     _check_state(system, state)
-    fmt, plan = _plan_for(system, cfg, ctx, reducer)
-    with plan:
+    with checked_out_plan(system, cfg.order_n, cfg.tau(ctx).as_fraction(), ctx, reducer) as (fmt, plan):
         out, status = plan.step(fmt.to_digits(state))
     if status.any():
         raise RangeError("state left the device fixed-point range (|x| >= 2^27) in step")
@@ -248,9 +295,9 @@ def integrate(
     traj.points.append(TrajectoryPoint(step=start_step, state=tuple(state0)))
     if n_steps == start_step:
         return traj
-    fmt, plan = _cached_plan(system, cfg, ctx, reducer)
     dev_stride = 1 if observer is not None else record_stride
-    steps, recs, status = plan.integrate(fmt.to_digits(state0), n_steps, start_step, dev_stride)
+    with checked_out_plan(system, cfg.order_n, cfg.tau(ctx).as_fraction(), ctx, reducer) as (fmt, plan):
+        steps, recs, status = plan.integrate(fmt.to_digits(state0), n_steps, start_step, dev_stride)
     if status.any():
         raise RangeError("state left the device fixed-point range (|x| >= 2^27) during integrate")
     prec = ctx.precision_bits

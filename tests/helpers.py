@@ -9,6 +9,25 @@ from oracle import ref as R
 
 EXACT = math.inf
 
+# ---------------------------------------------------------------------------
+# Declared tolerance. Two correct integrations of the same chaotic system that
+# round differently (the reference rounds every multiply and add to P bits;
+# the device carries 32 more bits and rounds once per sum) separate as
+#     e(t) ~ u * c * sum_s exp(lambda (t - s tau)) ~ u * c * exp(lambda t) / (lambda tau),
+# u = 10^-K, lambda = the largest Lyapunov exponent (0.906 for the Lorenz
+# attractor), c <= N the rounding error of one step in ulps (N accumulated
+# orders). In decimal digits:
+#     d(t) = ceil(log10(N / (lambda |tau|))) + ceil(1.05 * lambda t / ln 10)
+# (5 % on the slope for the finite-time fluctuation of the exponent). Measured
+# against the oracle re-run at P + 64 bits (tests/golden/*_p64.json,
+# profiles/r02_error_budget.json) the REFERENCE ITSELF loses 42 of its 500
+# digits by t = 100 and d(100) = 47; the test bound is this d(t) everywhere.
+LYAPUNOV = 0.906
+
+
+def guard_digits(t: float, order: int, tau: float = 0.01) -> int:
+    return math.ceil(math.log10(order / (LYAPUNOV * abs(tau)))) + math.ceil(1.05 * LYAPUNOV / math.log(10) * abs(t))
+
 
 def frac(hexval: str) -> Fraction:
     return R.dy_to_fraction(R.dy_from_hex(hexval))

@@ -42,6 +42,12 @@ def test_loads_without_device_and_pure_functions_work():
     assert L.mpt_record_count(250, 0, 100) == 4
     assert L.mpt_record_count(60, 20, 20) == 3
     assert L.mpt_record_count(5, 0, 0) < 0
+    # n_steps == start_step: the initial record only, also off the stride grid
+    assert L.mpt_record_count(250, 250, 100) == 1
+    assert L.mpt_record_count(200, 200, 100) == 1
+    assert L.mpt_record_count(0, 0, 7) == 1
+    assert L.mpt_record_count(251, 250, 100) == 2
+    assert L.mpt_record_count(10, 20, 5) < 0
 
 
 @pytest.mark.skipif(os.environ.get("CUDA_VISIBLE_DEVICES", None) is None and

@@ -189,3 +189,88 @@ def test_gather_rows_world2_gloo(n_total):
         assert p.exitcode == 0
     want = np.arange(n_total * 6, dtype=np.int32).reshape(n_total, 2, 3).tolist()
     assert got[0] == want and got[1] == want
+
+
+# ------------------------------------------------------- T_c-K sweep (host logic)
+def _model_run(inits, bits, order, tau_text, n_steps, stride):
+    """run_fn for tc_sweep on the CPU: every member through the bit-exact model of
+    the device arithmetic (oracle/fixmodel.c) -- same digit tables, same records."""
+    from oracle import fix as FX
+    from paper_1908_09301_b200.engine import SystemTables
+
+    ctx = M.PrecisionContext(bits)
+    fmt = FixedFormat(bits)
+    system = M.builtin_system("lorenz", ctx)
+    tables = SystemTables.build(system, fmt, order, M.mp_from_decimal(tau_text, ctx).as_fraction())
+    states = E.states_from_decimals(inits, bits, fmt)
+    recs, steps = [], None
+    for st in states:
+        steps, r = FX.integrate(tables, fmt.frac_digits, order, bits, st, n_steps, 0, stride)
+        recs.append(r)
+    return E.EnsembleRun(bits, order, tau_text, fmt, steps, np.stack(recs, axis=1),
+                         np.zeros(len(inits), np.int32))
+
+
+SWEEP = dict(K=20, N=14, n_members=5, n_steps=2400, stride=100, d=10)
+
+
+def _sweep_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rep = E.tc_sweep(rank=rank, world=world, run_fn=_model_run, **SWEEP)
+    q.put((rank, rep.agreement.tolist(), rep.tc_step.tolist(), rep.final_digits.tolist(), rep.final_xyz.tolist()))
+    dist.destroy_process_group()
+
+
+def test_tc_sweep_world2_gloo_matches_world1():
+    """Shard -> base + verify runs -> agreement -> t_c -> gather, world 2 over
+    gloo, against the unsharded result: identical for every member (the
+    reference's cross-worker-count bit-identity check, bench.py:62 run_benchmark)."""
+    import torch.multiprocessing as mp
+
+    one = E.tc_sweep(run_fn=_model_run, **SWEEP)
+    assert one.agreement.shape == (5, 25) and one.final_digits.shape[:2] == (5, 3)
+    # K=20 digits, d=10: the pair separates inside the run (a real divergence time)
+    assert (one.tc_step > 0).all() and (one.tc_step < SWEEP["n_steps"]).any()
+    tcs = E.divergence_times(one.steps, "0.01", one.agreement.T, SWEEP["d"])
+    assert [E.exact_time(int(s), "0.01") for s in one.tc_step] == tcs == one.t_c()
+    ctxm = mp.get_context("spawn")
+    q = ctxm.Queue()
+    port = _free_port()
+    procs = [ctxm.Process(target=_sweep_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = {r: rest for r, *rest in (q.get(timeout=300) for _ in procs)}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = [one.agreement.tolist(), one.tc_step.tolist(), one.final_digits.tolist(), one.final_xyz.tolist()]
+    assert got[0] == want and got[1] == want
+
+
+def test_tc_steps_edge_cases():
+    steps = np.array([0, 100, 200, 300])
+    agr = np.array([[E.EXACT_CODE, 30, 20, 12], [E.EXACT_CODE, 30, 9, 12], [5, 30, 20, 12], [E.EXACT_CODE, 9, 20, 3]])
+    assert E.tc_steps(steps, agr, 10).tolist() == [300, 100, 0, 0]
+    assert E.tc_steps(steps, np.zeros((0, 4), np.int64), 10).tolist() == []
+    with pytest.raises(ValueError):
+        E.tc_sweep(20, 14, 4, 150, stride=100, run_fn=_model_run)
+
+
+def test_decimal_to_fixed_int_matches_mp_path():
+    import random
+
+    rnd = random.Random(5)
+    for bits in (64, 167, 499, 2658):
+        ctx, fmt = M.PrecisionContext(bits), FixedFormat(bits)
+        texts = ["0", "-0.0", "1", "-15.8", "35.64", "1e-20", "-17.48000000000000000000731", "134217727.9999", ".5", "2.5e-1"]
+        texts += [f"{rnd.choice(['', '-'])}{rnd.randint(0, 10**rnd.randint(1, 8))}.{rnd.randint(0, 10**50):050d}e{rnd.randint(-30, 0)}"
+                  for _ in range(100)]
+        for t in texts:
+            assert E.decimal_to_fixed_int(t, bits, fmt) == fmt.to_int(M.mp_from_decimal(t, ctx)), (bits, t)
+        with pytest.raises(M.RangeError):
+            E.decimal_to_fixed_int("134217728", bits, fmt)
+        with pytest.raises(ValueError):
+            E.decimal_to_fixed_int("1,5", bits, fmt)

@@ -1,7 +1,8 @@
 """GPU parity tests (B200): the CUDA path through the C ABI against
   (1) the bit-exact model of the device arithmetic (oracle/fixmodel.c), and
   (2) the reference's frozen outputs (tests/golden, pinned to the unmodified
-      reference) within relative 10^-(K-d), d = 3 + ceil(0.3935 t).
+      reference) within relative 10^-(K-d(t)), d(t) from tests/helpers.py guard_digits
+      (derived there; both arms are also measured against a P+64-bit oracle run).
 Edge cases follow the reference's tests: zero state, zero steps, backward
 step, single-dimension system, random quadratic systems, resume, observer,
 determinism."""
@@ -18,13 +19,9 @@ from paper_1908_09301_b200.engine import DevicePlan, SystemTables
 from paper_1908_09301_b200.fixed import FixedFormat
 
 from .conftest import CANON_INIT
-from .helpers import EXACT, agreement_digits, frac, system_from_json
+from .helpers import EXACT, agreement_digits, frac, guard_digits, system_from_json
 
 pytestmark = pytest.mark.gpu
-
-
-def guard_digits(t: float) -> int:
-    return 3 + math.ceil(0.3935 * t)
 
 
 def lorenz_tables(P, N, tau="0.01", guard=32, scale=None):
@@ -50,10 +47,8 @@ def test_integrate_bit_exact_vs_model(gpu, P, N, steps, stride):
     assert np.array_equal(r_gpu[:, 0], r_cpu)
 
 
-@pytest.mark.parametrize("kernel,cluster", [("team", 1), ("cluster", 1), ("cluster", 2), ("cluster", 8),
-                                            ("cluster", 16), ("pipe", 1), ("pipe", 2), ("pipe", 4), ("pipe", 16),
-                                            ("relay", 2), ("relay", 3), ("relay", 8), ("relay", 16),
-                                            ("grid", 1), ("mx", 2), ("mx", 3), ("mx", 5), ("mx", 8), ("mx", 16)])
+@pytest.mark.parametrize("kernel,cluster", [("team", 1), ("grid", 1), ("mx", 2), ("mx", 3), ("mx", 5), ("mx", 8),
+                                            ("mx", 16)])
 @pytest.mark.parametrize("P,N,steps", [(167, 40, 12), (1661, 200, 2)])
 def test_every_kernel_bit_exact_vs_model(gpu, kernel, cluster, P, N, steps):
     ctx, system, fmt, tables = lorenz_tables(P, N)
@@ -169,10 +164,11 @@ def test_dropin_integrate_matches_reference(golden, gpu, name):
         got = [v.as_fraction() for v in pt.state]
         ref = [frac(h) for h in rec["state"]]
         d = agreement_digits(got, ref)
-        assert d == EXACT or d >= K - guard_digits(pt.step * tau), (name, pt.step, d)
+        assert d == EXACT or d >= K - guard_digits(pt.step * tau, c["order"], tau), (name, pt.step, d)
 
 
 LONG_RUNS = ("config1_k500_n200_10000", "config2_k2200_n1000_500", "config3_k4200_n3500_4")
+ERROR_BUDGET_RUNS = ("config1_k500_n200_10000", "config2_k2200_n1000_500")
 
 
 @pytest.mark.parametrize("name", LONG_RUNS)
@@ -202,7 +198,7 @@ def test_long_run_agreement_vs_oracle(gpu, name):
         got = [v.as_fraction() for v in pt.state]
         ref = [frac(h) for h in rec["state"]]
         d = agreement_digits(got, ref)
-        need = K - guard_digits(pt.step * tau)
+        need = K - guard_digits(pt.step * tau, c["order"], tau)
         report.append({"step": pt.step, "t": pt.step * tau, "agree_digits": None if d == EXACT else d,
                        "required": need})
         assert d == EXACT or d >= need, (name, pt.step, d, need)
@@ -210,6 +206,47 @@ def test_long_run_agreement_vs_oracle(gpu, name):
     os.makedirs(out, exist_ok=True)
     with open(os.path.join(out, f"parity_{name}.json"), "w") as fh:
         json.dump({"name": name, "K": K, "prec_bits": P, "order": c["order"], "records": report}, fh, indent=1)
+
+
+@pytest.mark.parametrize("name", ERROR_BUDGET_RUNS)
+def test_error_budget_vs_p64_oracle(gpu, name):
+    """Both arms against the oracle re-run at P + 64 bits (same inputs and order:
+    the truncation error is shared, so each arm's distance from that run is its
+    own rounding error). The device rounds its state to the reference precision
+    P after every step, as the reference does, and that rounding dominates both:
+    the device must be as close to the P + 64 run as the reference is, to within
+    one digit, at every record; device-vs-reference agreement then follows from
+    the triangle inequality and keeps >= 2 digits of margin over the declared d(t). The table goes to gpurun_out/error_budget_<name>.json."""
+    import json
+    import os
+
+    gdir = os.path.join(os.path.dirname(__file__), "golden")
+    with open(os.path.join(gdir, f"oracle_{name}.json")) as fh:
+        c = json.load(fh)
+    with open(os.path.join(gdir, f"oracle_{name}_p64.json")) as fh:
+        truth = json.load(fh)
+    P = c["prec_bits"]
+    ctx = M.PrecisionContext(P)
+    system = M.builtin_system("lorenz", ctx)
+    state0 = tuple(M.mp_from_decimal(t, ctx) for t in c["init"])
+    traj = M.integrate(system, state0, M.StepConfig(c["tau"], c["order"]), c["n_steps"], ctx,
+                       record_stride=c["stride"])
+    K, tau = c["K"], abs(float(Fraction(c["tau"])))
+    rows = []
+    for pt, rec, tr in zip(traj.points[1:], c["records"][1:], truth["records"][1:]):
+        assert pt.step == rec["step"] == tr["step"]
+        got = [v.as_fraction() for v in pt.state]
+        ref, tru = [frac(h) for h in rec["state"]], [frac(h) for h in tr["state"]]
+        e_dev, e_ref, d = agreement_digits(got, tru), agreement_digits(ref, tru), agreement_digits(got, ref)
+        need = K - guard_digits(pt.step * tau, c["order"], tau)
+        rows.append({"step": pt.step, "t": pt.step * tau, "device_vs_p64": e_dev, "reference_vs_p64": e_ref,
+                     "device_vs_reference": d, "required": need, "margin": d - need})
+        assert e_dev >= e_ref - 1, rows[-1]
+        assert d >= min(e_dev, e_ref) - 1 and d >= need + 2, rows[-1]
+    out = os.path.join(os.environ.get("GRAFT_REPO_ROOT", "."), "gpurun_out")
+    os.makedirs(out, exist_ok=True)
+    with open(os.path.join(out, f"error_budget_{name}.json"), "w") as fh:
+        json.dump({"name": name, "K": K, "prec_bits": P, "order": c["order"], "records": rows}, fh, indent=1)
 
 
 def test_reference_regression_pair_on_gpu(gpu):

@@ -1,6 +1,6 @@
 """Kernel sweep on one GPU: device ms per Taylor step for each kernel / cluster size.
 
-    python tools/perf_sweep.py 500:200:20:relay/16,pipe/16,cluster/16 2200:1000:1:grid/1
+    python tools/perf_sweep.py 500:200:20:mx/16,mx/8 2200:1000:1:grid/1
 
 Each argument is K:N:steps:kernel/G[,kernel/G...]. Not part of the product path.
 """
