@@ -51,9 +51,10 @@ def compute_jet(tables, frac_digits: int, order: int, state: np.ndarray, variant
                 bulk: int | None = None) -> np.ndarray:
     """-> coef[dim, order+1, W] (digits), exactly as the kernel computes them.
 
-    variant 0: per-order C-product recurrence (team/cluster/pipe/relay/grid
-    kernels); variant 1: matrix recurrence (mx kernel) with `bulk` bulk CTAs
-    (the partition of the Cauchy sums enters its rounding)."""
+    variant 0: per-order C-product recurrence (team and grid kernels);
+    variant 1: matrix recurrence (mx kernel) with `bulk` bulk CTAs (the partition
+    of the Cauchy sums enters its rounding); variant 2: value-exact matrix
+    recurrence; variant 3: value-exact per-order recurrence (warp kernel)."""
     _bulk(bulk)
     W = frac_digits + 1
     nt, k = _tables(tables)

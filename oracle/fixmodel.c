@@ -621,8 +621,66 @@ static int jet_lx(const model_t *M, int32_t *coef) {
   return rc;
 }
 
+/* ---------------------------------------------------------------------------
+ * Value-exact direct recurrence (variant 3; paper_1908_09301_b200/csrc/taylor_warp.cu,
+ * one warp per trajectory). The per-order recurrence of variant 0 with every
+ * rounding a function of the VALUE of an exact column sum only (sd_cols), so
+ * the device may skip zero digits, fold and reduce its partial sums in any
+ * order and still agree bit for bit:
+ *
+ *   a~_0^m   = sd(state^m)                                    (same value, recoded)
+ *   U_i^m    = rndb( [i==0] cst_m B^2 + sum_j tprod(lin[m][j], a~_i^j)
+ *                    + sum_{t in m} q_t sum_{k=0..i} tprod(a~^a_{i-k}, a~^b_k) )
+ *   a~_{i+1}^m = rndb( tprod(U_i^m, C_i, Lf+sc-2) )
+ * (tprod without a T argument: T = Lf-2.) Requires small-integer bilinear
+ * coefficients. The state update is the exact row sum rounded to P bits, as in
+ * every variant.
+ */
+static int jet_wp(const model_t *M, int32_t *coef) {
+  int Lf = M->Lf, L = Lf + 1, Wd = W(M), D = M->D, N = M->order;
+  int ncols = Lf + 4;
+  int64_t qint[64];
+  for (int t = 0; t < M->NT; t++)
+    if (!small_int(M->q + (size_t)t * Wd, Lf, &qint[t])) return -5;
+  i128 *col = malloc(sizeof(i128) * (size_t)(ncols + 8));
+  i128 *acc = malloc(sizeof(i128) * (size_t)(ncols + 8));
+  int32_t *U = malloc(sizeof(int32_t) * (size_t)D * Wd);
+  int rc = 0;
+#define CO(m, i) (coef + ((size_t)(m) * (N + 1) + (i)) * Wd)
+  for (int m = 0; m < D && !rc; m++) {
+    for (int d = 0; d <= Lf; d++) acc[d] = CO(m, 0)[d];
+    if (sd_cols(acc, Wd, 0, 0, Wd, CO(m, 0))) rc = 1;
+  }
+  for (int i = 0; i < N && !rc; i++) {
+    for (int m = 0; m < D; m++) {
+      memset(col, 0, sizeof(i128) * ncols);
+      if (i == 0)
+        for (int j = 0; j <= Lf; j++) col[2 + j] += (i128)M->cst[(size_t)m * Wd + j];
+      for (int j = 0; j < D; j++) tprod_acc(M->lin + ((size_t)m * D + j) * Wd, CO(j, i), L, Lf - 2, col, ncols);
+      for (int t = 0; t < M->NT; t++) {
+        if (M->teq[t] != m) continue;
+        memset(acc, 0, sizeof(i128) * ncols);
+        for (int k = 0; k <= i; k++) tprod_acc(CO(M->tj[t], i - k), CO(M->tk[t], k), L, Lf - 2, acc, ncols);
+        for (int c = 0; c < ncols; c++) col[c] += (i128)qint[t] * acc[c];
+      }
+      if (rndb(col, ncols, Wd, U + (size_t)m * Wd)) rc = 1;
+    }
+    for (int m = 0; m < D; m++) {
+      memset(col, 0, sizeof(i128) * ncols);
+      tprod_acc(U + (size_t)m * Wd, M->ctab + (size_t)i * Wd, L, Lf + M->sc - 2, col, ncols);
+      if (rndb(col, ncols, Wd, CO(m, i + 1))) rc = 1;
+    }
+  }
+#undef CO
+  free(col);
+  free(acc);
+  free(U);
+  return rc;
+}
+
 static int jet_any(const model_t *M, int32_t *coef) {
-  return M->variant == 2 ? jet_lx(M, coef) : M->variant == 1 ? jet_mx(M, coef) : jet(M, coef);
+  return M->variant == 3 ? jet_wp(M, coef)
+         : M->variant == 2 ? jet_lx(M, coef) : M->variant == 1 ? jet_mx(M, coef) : jet(M, coef);
 }
 
 /* round the canonical digit vector to `prec` significant bits, ties to even */

@@ -25,6 +25,10 @@ size_t mx_scratch_bytes(const Params& p);
 bool mx_supported(const Params& p);
 cudaError_t launch_mx_kernel(const Params& p, int G, size_t smem, cudaStream_t stream);
 int mx_max_cluster(const Params& p, size_t smem, int want);
+bool warp_supported(const Params& p);
+size_t warp_traj_smem(const Params& p);
+int warp_choose_wpb(const Params& p, size_t smem_sm, size_t optin);
+cudaError_t launch_warp_kernel(const Params& p, int wpb, cudaStream_t stream);
 }  // namespace mpt
 
 static thread_local std::string g_err;
@@ -56,7 +60,9 @@ struct mpt_plan {
   bool have_constants = false;
   unsigned long long* d_counters = nullptr;
   bool counting = false;
-  int kernel = 0;    // 1 team (rows in HBM/L2), 4 grid (all SMs), 6 mx (matrix recurrence)
+  int kernel = 0;    // 1 team (rows in HBM/L2), 4 grid (all SMs), 6 mx (matrix recurrence), 7 warp (one warp per trajectory)
+  int warp_wpb = 0;  // warp kernel: trajectories (warps) per CTA
+  int smem_sm = 0;   // shared memory per SM
   int cluster = 1;   // CTAs per trajectory (mx), co-resident CTAs (grid)
   size_t smem_cluster = 0;
   int optin = 0;
@@ -114,6 +120,25 @@ static int choose_kernel(mpt_plan* pl, int kernel, int want) {
     pl->kernel = 4;
     pl->cluster = pl->grid_blocks;
     return MPT_OK;
+  }
+  // small precision (W <= 34 digits): one warp per trajectory, rows in shared memory
+  if ((kernel == 7 || (kernel == 0 && (p.n_traj > 1 || !mpt::mx_supported(p)))) && pl->have_constants &&
+      mpt::warp_supported(p)) {
+    const int wpb = mpt::warp_choose_wpb(p, (size_t)pl->smem_sm, (size_t)pl->optin);
+    if (wpb > 0) {
+      pl->kernel = 7;
+      pl->cluster = 1;
+      pl->warp_wpb = p.n_traj < wpb ? p.n_traj : wpb;
+      pl->smem_cluster = mpt::warp_traj_smem(p) * pl->warp_wpb;
+      return MPT_OK;
+    }
+  }
+  if (kernel == 7) {
+    if (!pl->have_constants) {
+      pl->kernel = 0;
+      return MPT_OK;
+    }
+    return fail(MPT_EUNSUP, "the warp kernel does not support this system/precision (W <= 34 digits, integer bilinear coefficients, rows in shared memory)");
   }
   const int tries[] = {16, 8, 4, 2, 1};
   // the matrix-recurrence kernel (lead CTA + bulk CTAs, K table in global memory)
@@ -279,6 +304,7 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     pl->nsm = nsm;
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+    pl->smem_sm = smem_sm;
     const char* em = getenv("MPT_TEAM_MB");
     // four 128-thread CTAs per SM for small digit counts (latency bound), two otherwise
     const int want_mb = em ? atoi(em) : (n_traj >= 8 * nsm && p.W <= 20 ? 8 : n_traj >= 4 * nsm && p.W <= 64 ? 4 : n_traj >= 2 * nsm ? 2 : 1);
@@ -345,6 +371,7 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
     int kernel = ek ? (strcmp(ek, "team") == 0   ? 1
                        : strcmp(ek, "grid") == 0 ? 4
                        : strcmp(ek, "mx") == 0   ? 6
+                       : strcmp(ek, "warp") == 0 ? 7
                                                  : 0)
                     : 0;
     int want = ec ? atoi(ec) : (n_traj == 1 ? 16 : 1);
@@ -359,7 +386,7 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
 }
 
 int mpt_plan_configure(mpt_plan* pl, int kernel, int cluster) {
-  if (!pl || (kernel != 0 && kernel != 1 && kernel != 4 && kernel != 6) || cluster < 1 || cluster > 16)
+  if (!pl || (kernel != 0 && kernel != 1 && kernel != 4 && kernel != 6 && kernel != 7) || cluster < 1 || cluster > 16)
     return fail(MPT_EINVAL, "bad configuration");
   return choose_kernel(pl, kernel, cluster);
 }
@@ -401,7 +428,7 @@ int mpt_plan_info(const mpt_plan* pl, int* smem_bytes, int* k_chunk, int* thread
     k_chunk = nullptr;
   }
   if (k_chunk) *k_chunk = pl->p.kc;
-  if (threads) *threads = pl->p.nthreads;
+  if (threads) *threads = pl->kernel == 7 ? 32 * pl->warp_wpb : pl->p.nthreads;
   return MPT_OK;
 }
 
@@ -499,6 +526,8 @@ static int launch(mpt_plan* pl, int n_steps, int start_step, int stride, cudaStr
     CK(cudaMemsetAsync(pl->d_status, 0, sizeof(int32_t) * p.n_traj, stream));
     p.gscratch = pl->d_mxscratch;
     CK(mpt::launch_mx_kernel(p, pl->cluster, pl->smem_cluster, stream));
+  } else if (pl->kernel == 7) {
+    CK(mpt::launch_warp_kernel(p, pl->warp_wpb, stream));
   } else {
     CK(mpt::launch_team_kernel(p, pl->smem, stream));
   }

@@ -52,7 +52,7 @@ class SystemTables:
         )
 
 
-KERNEL_NAMES = {1: "team", 4: "grid", 6: "mx"}  # include/mptaylor_b200.h mpt_plan_configure
+KERNEL_NAMES = {1: "team", 4: "grid", 6: "mx", 7: "warp"}  # include/mptaylor_b200.h mpt_plan_configure
 
 
 def _p(a: np.ndarray):
@@ -115,10 +115,9 @@ class DevicePlan:
     @property
     def variant(self) -> int:
         """Arithmetic variant of the selected kernel (oracle/fixmodel.c): 1 for the
-        matrix-recurrence kernel, 0 for the per-order C-product kernels."""
-        kern, cl = ctypes.c_int32(), ctypes.c_int32()
-        _native.check(self.lib.mpt_plan_kernel(self.h, ctypes.byref(kern), ctypes.byref(cl)))
-        return 1 if kern.value == 6 else 0
+        matrix-recurrence kernel, 3 for the warp kernel (value-exact roundings), 0
+        for the per-order C-product kernels (team, grid)."""
+        return self.model_kwargs()["variant"]
 
     def model_kwargs(self) -> dict:
         """Arguments that make oracle/fixmodel.c reproduce this plan's kernel bit for
@@ -129,6 +128,8 @@ class DevicePlan:
         _native.check(self.lib.mpt_plan_kernel(self.h, ctypes.byref(kern), ctypes.byref(cl)))
         if kern.value == 6:
             return {"variant": 1, "bulk": cl.value - 1}
+        if kern.value == 7:
+            return {"variant": 3}
         return {"variant": 0}
 
     def configure(self, kernel: str = "auto", cluster: int = 8):

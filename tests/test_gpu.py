@@ -47,7 +47,7 @@ def test_integrate_bit_exact_vs_model(gpu, P, N, steps, stride):
     assert np.array_equal(r_gpu[:, 0], r_cpu)
 
 
-@pytest.mark.parametrize("kernel,cluster", [("team", 1), ("grid", 1), ("mx", 2), ("mx", 3), ("mx", 5), ("mx", 8),
+@pytest.mark.parametrize("kernel,cluster", [("team", 1), ("warp", 1), ("grid", 1), ("mx", 2), ("mx", 3), ("mx", 5), ("mx", 8),
                                             ("mx", 16)])
 @pytest.mark.parametrize("P,N,steps", [(167, 40, 12), (1661, 200, 2)])
 def test_every_kernel_bit_exact_vs_model(gpu, kernel, cluster, P, N, steps):
@@ -127,6 +127,28 @@ def test_team_kernel_two_ctas_per_sm_bit_exact(gpu, monkeypatch, mb, K, N, steps
     for j in (0, 3, n_traj - 1):
         _, r_cpu = FX.integrate(tables, fmt.frac_digits, N, P, states[j], steps, 0, 1, **kw)
         assert np.array_equal(r_gpu[:, j], r_cpu), j
+
+
+@pytest.mark.parametrize("K,N,steps,n_traj", [(20, 14, 40, 2), (50, 40, 30, 1), (100, 60, 8, 9), (150, 90, 4, 5),
+                                              (200, 120, 3, 37), (250, 150, 2, 3), (270, 20, 3, 2)])
+def test_warp_kernel_bit_exact(gpu, K, N, steps, n_traj):
+    """One warp per trajectory (W <= 34 digits; one or two columns per lane, every
+    product-window width): records and the jet bit-exact vs the value-exact model."""
+    P = M.bits_for_digits(K)
+    ctx, system, fmt, tables = lorenz_tables(P, N)
+    base = [M.mp_from_decimal(t, ctx).as_fraction() for t in CANON_INIT]
+    states = np.stack([fmt.to_digits([b + Fraction(5 * j - 7, 10**18) for b in base]) for j in range(n_traj)])
+    with DevicePlan(tables, fmt, N, n_traj) as plan:
+        plan.configure("warp", 1)
+        assert plan.info()["kernel"] == "warp"
+        _, r_gpu, status = plan.integrate(states, steps, 0, 1)
+        jets = plan.compute_jet(states)
+        kw = plan.model_kwargs()
+    assert kw == {"variant": 3} and not status.any()
+    for j in sorted({0, n_traj // 2, n_traj - 1}):
+        _, r_cpu = FX.integrate(tables, fmt.frac_digits, N, P, states[j], steps, 0, 1, **kw)
+        assert np.array_equal(r_gpu[:, j], r_cpu), j
+        assert np.array_equal(jets[j], FX.compute_jet(tables, fmt.frac_digits, N, states[j], **kw)), j
 
 
 def test_random_quadratic_systems_jets_bit_exact(golden, gpu):

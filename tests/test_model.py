@@ -26,7 +26,8 @@ def _small_int_q(tables):
     return [not r[:Lf].any() and abs(int(r[Lf])) <= 4096 for r in tables.q]
 
 
-VARIANTS = [0, 1, 2]  # 0: per-order C-product recurrence, 1: matrix recurrence (mx kernel), 2: value-exact (lx kernel)
+VARIANTS = [0, 1, 2, 3]  # 0: per-order C-product recurrence, 1: matrix recurrence (mx kernel), 2: value-exact matrix
+# recurrence (lx kernel), 3: value-exact per-order recurrence (warp kernel)
 
 
 def run_model(case, guard_bits=32, variant=0):
