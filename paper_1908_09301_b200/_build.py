@@ -10,13 +10,15 @@ gpurun snapshot).
 from __future__ import annotations
 
 import os
+import re
 import shutil
 import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
-SOURCES = ("csrc/taylor_kernel.cu", "csrc/taylor_grid.cu", "csrc/taylor_mx.cu", "csrc/taylor_warp.cu", "csrc/capi.cu")
+SOURCES = ("csrc/taylor_kernel.cu", "csrc/taylor_grid.cu", "csrc/taylor_mx.cu", "csrc/taylor_warp.cu", "csrc/taylor_warp2.cu",
+           "csrc/capi.cu")
 OUT = os.path.join(HERE, "_lib", "libmptaylor_b200.so")
 ARCH = ("-gencode", "arch=compute_100a,code=sm_100a")
 
@@ -40,15 +42,24 @@ def build(verbose: bool = False, extra=(), incremental: bool = False) -> str:
               "-I", os.path.join(REPO, "include"), *(["-Xptxas", "-v"] if verbose else []), *extra]
 
     csrc = os.path.join(HERE, "csrc")
-    deps = [os.path.join(csrc, f) for f in os.listdir(csrc) if f.endswith(".cuh")]
-    deps.append(os.path.join(REPO, "include", "mptaylor_b200.h"))
-    dep_mtime = max(os.path.getmtime(d) for d in deps)
+
+    def newest(path, seen):
+        """Latest mtime of a source and of every header it includes (quoted includes, recursively)."""
+        if path in seen or not os.path.exists(path):
+            return 0.0
+        seen.add(path)
+        t = os.path.getmtime(path)
+        with open(path) as fh:
+            for line in fh:
+                m = re.match(r'\s*#\s*include\s+"([^"]+)"', line)
+                if m:
+                    t = max(t, newest(os.path.normpath(os.path.join(os.path.dirname(path), m.group(1))), seen))
+        return t
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
-        # incremental: an object newer than its source and every header is reused
-        if (incremental and os.path.exists(obj)
-                and os.path.getmtime(obj) > max(os.path.getmtime(os.path.join(HERE, src)), dep_mtime)):
+        # incremental: an object newer than its source and every header it includes is reused
+        if incremental and os.path.exists(obj) and os.path.getmtime(obj) > newest(os.path.join(HERE, src), set()):
             return obj, ""
         res = subprocess.run([*common, "-c", "-o", obj, os.path.join(HERE, src)], capture_output=True, text=True)
         if res.returncode != 0:
