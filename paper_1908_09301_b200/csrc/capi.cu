@@ -122,8 +122,7 @@ static int choose_kernel(mpt_plan* pl, int kernel, int want) {
     return MPT_OK;
   }
   // small precision (W <= 34 digits): one warp per trajectory, rows in shared memory
-  if ((kernel == 7 || (kernel == 0 && (p.n_traj > 1 || !mpt::mx_supported(p)))) && pl->have_constants &&
-      mpt::warp_supported(p)) {
+  if ((kernel == 0 || kernel == 7) && pl->have_constants && mpt::warp_supported(p)) {
     const int wpb = mpt::warp_choose_wpb(p, (size_t)pl->smem_sm, (size_t)pl->optin);
     if (wpb > 0) {
       pl->kernel = 7;

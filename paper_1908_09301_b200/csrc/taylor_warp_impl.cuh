@@ -436,6 +436,31 @@ __global__ void __launch_bounds__(128, MINB) taylor_warp_kernel(const __grid_con
     }
   }
 
+  // per-kernel tables in registers: integer multiplier of pair q in equation m, integer
+  // linear coefficients, and which linear entries need a full product (bit m*DT + jv)
+  int pm[NG][DT], linint[DT][DT];
+  unsigned bigmask = 0;
+#pragma unroll
+  for (int m = 0; m < DT; m++) {
+#pragma unroll
+    for (int q = 0; q < NG; q++) {
+      int s = 0;
+      for (int t = 0; t < p.NT; t++)
+        if (p.tpair[t] == q && p.teq[t] == m) s += p.tq_int[t];
+      pm[q][m] = s;
+    }
+#pragma unroll
+    for (int jv = 0; jv < DT; jv++) {
+      linint[m][jv] = 0;
+      if (m < D && jv < D) {
+        if (p.lin_small[m * D + jv])
+          linint[m][jv] = p.lin_int[m * D + jv];
+        else
+          bigmask |= 1u << (m * DT + jv);
+      }
+    }
+  }
+
   Ctx cx{rows, zt, L.stride, N1, Lf, p.NP};
   MacCount mcount;
   MacCount* mc = p.counters ? &mcount : nullptr;
@@ -489,38 +514,38 @@ __global__ void __launch_bounds__(128, MINB) taylor_warp_kernel(const __grid_con
 #pragma unroll
         for (int j = 0; j < MC; j++) U[m][j] = i == 0 ? (int64_t)cstreg[m][j] : 0;
       }
-      {
+#pragma unroll
+      for (int m = 0; m < DT; m++)
+#pragma unroll
+        for (int jv = 0; jv < DT; jv++)
+          if (linint[m][jv] != 0) {
+#pragma unroll
+            for (int j = 0; j < MC; j++) U[m][j] += (int64_t)linint[m][jv] * rowreg[jv][j];
+          }
+      if (bigmask) {
         int slot = 0;
 #pragma unroll
         for (int m = 0; m < DT; m++) {
 #pragma unroll
           for (int jv = 0; jv < DT; jv++) {
-            if (m < D && jv < D) {
-              const int e = m * D + jv;
-              if (p.lin_small[e]) {
-                const int kq = p.lin_int[e];
-                if (kq != 0) {
+            if (bigmask & (1u << (m * DT + jv))) {
+              // tprod(lin[m][jv], a~_i^jv): row digits broadcast from shared memory
+              const int32_t* ar = rows + (size_t)(jv * N1 + i) * L.stride;
+              const int wa = W - zt[jv * N1 + i];  // digits above are zero
+              const int32_t* lb[MC];
 #pragma unroll
-                  for (int j = 0; j < MC; j++) U[m][j] += (int64_t)kq * rowreg[jv][j];
-                }
-              } else {
-                // tprod(lin[m][jv], a~_i^jv): row digits broadcast from shared memory
-                const int32_t* ar = rows + (size_t)(jv * N1 + i) * L.stride;
-                const int32_t* lb = lbuf + (size_t)slot * L.bw;
-                const int wa = W - zt[jv * N1 + i];  // digits above are zero
-#pragma unroll 2
-                for (int pp = 0; pp < wa; pp++) {
-                  const int32_t a = ar[pp];
+              for (int j = 0; j < MC; j++) lb[j] = lbuf + (size_t)slot * L.bw + (okc[j] ? lane * MC + j + T : -4);
+#pragma unroll 4
+              for (int pp = 0; pp < wa; pp++) {
+                const int32_t a = ar[pp];
 #pragma unroll
-                  for (int j = 0; j < MC; j++)
-                    if (okc[j]) U[m][j] = madw(a, lb[lane * MC + j + T - pp], U[m][j]);
-                }
-                if (mc) {
-                  mc->executed += (unsigned long long)wa;
-                  mc->useful += (unsigned long long)wa / 2 + 1;
-                }
-                slot++;
+                for (int j = 0; j < MC; j++) U[m][j] = madw(a, lb[j][okc[j] ? -pp : 0], U[m][j]);
               }
+              if (mc) {
+                mc->executed += (unsigned long long)wa;
+                mc->useful += (unsigned long long)wa / 2 + 1;
+              }
+              slot++;
             }
           }
         }
@@ -534,12 +559,9 @@ __global__ void __launch_bounds__(128, MINB) taylor_warp_kernel(const __grid_con
           if (q < p.NP) {
 #pragma unroll
             for (int m = 0; m < DT; m++) {
-              int mult = 0;
-              for (int t = 0; t < p.NT; t++)
-                if (p.tpair[t] == q && p.teq[t] == m) mult += p.tq_int[t];
-              if (mult != 0) {
+              if (pm[q][m] != 0) {
 #pragma unroll
-                for (int j = 0; j < MC; j++) U[m][j] += (int64_t)mult * colv[q][j];
+                for (int j = 0; j < MC; j++) U[m][j] += (int64_t)pm[q][m] * colv[q][j];
               }
             }
           }
@@ -565,13 +587,23 @@ __global__ void __launch_bounds__(128, MINB) taylor_warp_kernel(const __grid_con
       for (int m = 0; m < DT; m++)
 #pragma unroll
         for (int j = 0; j < MC; j++) x[m][j] = 0;
-#pragma unroll 2
-      for (int pp = 0; pp < W; pp++) {
-        const int4 a4 = *(const int4*)(ubuf + 4 * pp);
+      {
+        // columns >= ncols read the low zero padding (index -4): no predicates in the loop
+        const int32_t* bq[MC];
+        int step[MC];
 #pragma unroll
         for (int j = 0; j < MC; j++) {
-          if (okc[j]) {
-            const int32_t b = bbuf[lane * MC + j + Tc - pp];
+          bq[j] = bbuf + (okc[j] ? lane * MC + j + Tc : -4);
+          step[j] = okc[j] ? 1 : 0;
+        }
+        const int4* up = (const int4*)ubuf;
+#pragma unroll 4
+        for (int pp = 0; pp < W; pp++) {
+          const int4 a4 = up[pp];
+#pragma unroll
+          for (int j = 0; j < MC; j++) {
+            const int32_t b = *bq[j];
+            bq[j] -= step[j];
             x[0][j] = madw(a4.x, b, x[0][j]);
             if (DT > 1) x[1][j] = madw(a4.y, b, x[1][j]);
             if (DT > 2) x[2][j] = madw(a4.z, b, x[2][j]);
