@@ -64,16 +64,17 @@ int mpt_plan_create(mpt_plan **plan, int dim, int nterms, const int32_t *term_eq
                     int order, int prec_bits, int n_traj, int device);
 int mpt_plan_destroy(mpt_plan *plan);
 
-/* Kernel selection (default: automatic -- single trajectories use the
- * pipelined cluster kernel (rows resident in distributed smem, up to 16 CTAs)
- * when the system fits it, else the cluster kernel, else the grid kernel on all
- * SMs; ensembles use the team kernel, one CTA per trajectory).
- * kernel: 0 auto, 1 team (rows in HBM/L2), 2 cluster (rows in smem),
- *         3 pipelined cluster kernel (warp-specialised lookahead, single trajectories),
- *         4 grid kernel (one trajectory on every SM, rows in L2; large precision);
- * cluster: CTAs per trajectory (1..16) for the cluster kernel.
- * Environment overrides at plan creation: MPT_KERNEL=team|cluster|pipe|grid, MPT_CLUSTER=G,
- * MPT_TEAM_MB=1|2|4 (team kernel CTAs per SM; default 4 (128 threads) when n_traj >= 4 x SMs and W <= 64, else 2 when n_traj >= 2 x SMs). */
+/* Kernel selection (default 0 = automatic):
+ *   W <= 34 digits, integer bilinear coefficients, rows fit shared memory
+ *                      -> 7 warp kernel (one warp per trajectory; ensembles and small
+ *                         single trajectories)
+ *   one trajectory     -> 6 mx (matrix recurrence on a 16-CTA cluster, W <= 120 digits),
+ *                         else 4 grid kernel (one trajectory on every SM, rows in L2)
+ *   ensembles          -> 1 team kernel (one CTA per trajectory, rows in HBM/L2)
+ * kernel: 0 auto, 1 team, 4 grid, 6 mx, 7 warp; cluster: CTAs per trajectory (2..16) for mx.
+ * Environment overrides at plan creation: MPT_KERNEL=team|grid|mx|warp, MPT_CLUSTER=G,
+ * MPT_TEAM_MB=1|2|4|8 (team kernel CTAs per SM; default 8 (64 threads) when n_traj >= 8 x SMs
+ * and W <= 20, 4 (128 threads) when n_traj >= 4 x SMs and W <= 64, 2 when n_traj >= 2 x SMs). */
 int mpt_plan_configure(mpt_plan *plan, int kernel, int cluster);
 int mpt_plan_kernel(const mpt_plan *plan, int *kernel, int *cluster);
 

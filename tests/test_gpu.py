@@ -381,3 +381,25 @@ def test_overflow_is_reported_not_silent(gpu):
     with pytest.raises(Exception) as info:
         M.integrate(system, (ctx.from_int(10**5),), M.StepConfig("1", 20), 3, ctx)
     assert "range" in str(info.value).lower()
+
+
+def test_reference_side_binding_stub(gpu):
+    """examples/reference_binding.py (the ctypes stub INTEGRATION.md shows for the
+    reference package) drives the C ABI on its own and returns the records of
+    the drop-in integrate() bit for bit."""
+    import importlib.util
+    import os
+
+    from paper_1908_09301_b200 import _native
+
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "examples", "reference_binding.py")
+    spec = importlib.util.spec_from_file_location("reference_binding", path)
+    stub = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(stub)
+    ctx, system, state = _lorenz(200)
+    recs = stub.integrate_b200(_native.LIB_PATH, system, state, "0.01", 24, 250, 200, record_stride=100)
+    traj = M.integrate(system, state, M.StepConfig("0.01", 24), 250, ctx, record_stride=100)
+    assert [s for s, _ in recs] == traj.steps() == [0, 100, 200, 250]
+    for (_, row), pt in zip(recs, traj.points):
+        for (num, fb), v in zip(row, pt.state):
+            assert Fraction(num, 1 << fb) == v.as_fraction()
