@@ -292,8 +292,8 @@ def tc_sweep(K: int, N: int, n_members: int, n_steps: int, rank: int = 0, world:
         agr = agreement_matrix(base, ver).T.copy()  # [members, nrec]
         tc_step = tc_steps(steps, agr, d)
         final_digits = np.ascontiguousarray(base.records[-1])
-        scale = 2.0 ** (-base.fmt.frac_bits)
-        final_xyz = np.array([[x * scale for x in row] for row in base.ints(base.records.shape[0] - 1)], np.float64)
+        one = 1 << base.fmt.frac_bits  # int / int: correctly rounded, no float overflow at large F
+        final_xyz = np.array([[x / one for x in row] for row in base.ints(base.records.shape[0] - 1)], np.float64)
         kms = {"base": base.kernel_ms, "verify": ver.kernel_ms}
     else:  # more ranks than members: an empty shard still takes part in the gather
         fmt = FixedFormat(bb)
