@@ -33,6 +33,21 @@ def _to_fixed(value, frac_bits: int) -> int:
     return _round_div(int(n) << frac_bits, int(d))
 
 
+def _round_to_bits(fr: Fraction, bits: int) -> Fraction:
+    """fr rounded to `bits` significant bits, ties to even (what mpfr(text, precision) does)."""
+    if fr == 0:
+        return fr
+    n, d = abs(fr.numerator), fr.denominator
+    s = bits + d.bit_length() - n.bit_length() + 1
+    for _ in range(3):
+        q = _round_div(n << s, d) if s >= 0 else _round_div(n, d << -s)
+        if q.bit_length() <= bits:
+            break
+        s -= 1
+    val = Fraction(q, 1 << s) if s >= 0 else Fraction(q << -s)
+    return -val if fr < 0 else val
+
+
 def _digits(x: int, width: int) -> list:
     sign, mag = (-1, -x) if x < 0 else (1, x)
     return [sign * ((mag >> (RADIX_BITS * j)) & ((1 << RADIX_BITS) - 1)) for j in range(width)]
@@ -68,7 +83,7 @@ def integrate_b200(lib_path, system, state0, tau_text, order, n_steps, prec_bits
     cst = arr(flat(system.constant))
     lin = arr(flat([v for row in system.linear for v in row]))
     q = arr(flat([t[3] for t in terms]) or [0] * width)
-    tau = Fraction(tau_text)
+    tau = _round_to_bits(Fraction(tau_text), prec_bits)  # the reference steps with tau rounded to P bits (taylor.py:234)
     c_shift = 1 if abs(tau) < Fraction(1, 4) else 0
     num = tau.numerator << (frac_bits + RADIX_BITS * c_shift)
     ctab = arr([d for i in range(order) for d in _digits(_round_div(num, tau.denominator * (i + 1)), width)])

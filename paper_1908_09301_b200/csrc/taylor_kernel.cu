@@ -36,6 +36,12 @@ struct Geo {
   int NCX;           // column-sum length (relative to T), covers all groups + carry
 };
 
+// Phase A partial columns: one padding slot after every 8 columns and an odd unit
+// stride, so the lanes of a warp (8-column windows 64 bytes apart, units NCX
+// apart) spread over the shared-memory banks instead of piling on two of them.
+__host__ __device__ inline int part_idx(int c) { return c + (c >> 3); }
+__host__ __device__ inline int part_stride(int NCX) { return (NCX + NCX / 8 + 1) | 1; }
+
 __host__ __device__ inline Geo make_geo(const Params& p) {
   Geo g;
   g.Tb = p.Lf - 2;
@@ -91,7 +97,7 @@ __host__ __device__ inline Layout make_layout(const Params& p) {
   L.off_uinf = take(sizeof(int2) * (size_t)p.D);
   L.off_ct = take(sizeof(int32_t) * (size_t)L.rw);
   L.off_ctinf = take(sizeof(int2));
-  L.off_part = take(sizeof(int64_t) * (size_t)L.n_units * g.NCX);
+  L.off_part = take(sizeof(int64_t) * (size_t)L.n_units * part_stride(g.NCX));
   L.off_col = take(sizeof(int64_t) * (size_t)(p.NP + p.D) * g.NCX);  // V_p then U_m
   L.off_uout = take(sizeof(int) * (size_t)L.n_units);
   L.off_flag = take(sizeof(int) * 4);
@@ -258,29 +264,30 @@ __global__ void __launch_bounds__(MB >= 8 ? 64 : MB >= 4 ? 128 : 256, MB) taylor
           __syncthreads();
         }
         // partials: unit = slot * NP + q, columns relative to Tb
+        const int pst = part_stride(g.NCX);
         if (active) {
-          int64_t* pr = part + (size_t)(slot * p.NP + q) * g.NCX;
+          int64_t* pr = part + (size_t)(slot * p.NP + q) * pst;
           acc_fold(accA, c0A, g.Tb);
 #pragma unroll
           for (int r = 0; r < kR; r++) {
             int c = c0A + r - g.Tb;
-            if (c >= 0) pr[c] = accA.v[r];
+            if (c >= 0) pr[part_idx(c)] = accA.v[r];
           }
           if (twoB) {
             acc_fold(accB, c0B, g.Tb);
 #pragma unroll
             for (int r = 0; r < kR; r++) {
               int c = c0B + r - g.Tb;
-              if (c >= 0) pr[c] = accB.v[r];
+              if (c >= 0) pr[part_idx(c)] = accB.v[r];
             }
           }
         }
         for (int u = tid; u < ns_a * p.NP; u += nt) uout[u] = u % p.NP;
         __syncthreads();
         if (active) {
-          int64_t* pr = part + (size_t)(slot * p.NP + q) * g.NCX;
-          pr[c0A + kR - g.Tb] += accA.v[kR];  // carries land in distinct columns (h+1 <= NGb-h)
-          if (twoB) pr[c0B + kR - g.Tb] += accB.v[kR];
+          int64_t* pr = part + (size_t)(slot * p.NP + q) * pst;
+          pr[part_idx(c0A + kR - g.Tb)] += accA.v[kR];  // carries land in distinct columns (h+1 <= NGb-h)
+          if (twoB) pr[part_idx(c0B + kR - g.Tb)] += accB.v[kR];
         }
         __syncthreads();
         // reduce units -> colsum[q][c]
@@ -288,12 +295,12 @@ __global__ void __launch_bounds__(MB >= 8 ? 64 : MB >= 4 ? 128 : 256, MB) taylor
         for (int e = tid; e < p.NP * ncol; e += nt) {
           int q = e / ncol, c = e % ncol;
           int64_t s = 0;
-          for (int sl = 0; sl < ns_a; sl++) s += part[(size_t)(sl * p.NP + q) * g.NCX + c];
+          for (int sl = 0; sl < ns_a; sl++) s += part[(size_t)(sl * p.NP + q) * pst + part_idx(c)];
           colsum[(size_t)q * g.NCX + c] = s;
         }
         // clear partials for the next use
         __syncthreads();
-        for (size_t w = tid; w < (size_t)ns_a * p.NP * g.NCX; w += nt) part[w] = 0;
+        for (size_t w = tid; w < (size_t)ns_a * p.NP * pst; w += nt) part[w] = 0;
         for (int q = warp; q < p.NP; q += nwarps) {
           if (!p.pair_round[q]) continue;
           bool o = warp_normalize(colsum + (size_t)q * g.NCX, ncol, 2, p.W, ROW(srow, q), &sinf[q], 0);

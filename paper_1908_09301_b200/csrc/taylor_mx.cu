@@ -47,6 +47,7 @@ constexpr int kPerWarpPass = 4;        // bulk products accumulated per lane bef
 constexpr int kQ = 16;                 // zero-skipping width quantum (digits)
 constexpr int kMaxQ = 4;               // widths up to 64 digits (K <= ~500): 2 x 4 x 4 product shapes
 constexpr int kShapes = 2 * kMaxQ * kMaxQ;
+constexpr int kScrStride = 33;         // int64 per column of a warp's window scratch (32 lanes + 1: bank spread)
 
 struct Geo {
   int W, KW, T, Tc, ncols, ncp, ng, rs, krs, urs;
@@ -141,7 +142,7 @@ __host__ __device__ inline Layout make_layout(const Params& p, int G) {
   L.off_recv = take(sizeof(int64_t) * 2 * (size_t)(L.Gb > 0 ? L.Gb : 1) * NPp * g.ncp);
   L.off_ssum = take(sizeof(int64_t) * (size_t)p.D * (g.W + 3));
   L.off_cinf = take(sizeof(int2) * (size_t)p.N);
-  L.off_scr = take(sizeof(int64_t) * (size_t)kWarps * 32 * 8);
+  L.off_scr = take(sizeof(int64_t) * (size_t)kWarps * kScrStride * 8);
   L.off_lshr = take(0);
   L.off_lshg = take(0);
   L.lead_total = o;
@@ -158,7 +159,7 @@ __host__ __device__ inline Layout make_layout(const Params& p, int G) {
   L.off_bcc = take(sizeof(int64_t) * (size_t)NPp * g.ncp);
   L.off_kst = take(sizeof(int32_t) * (size_t)kWarps * g.krs);
   L.off_kcol = take(sizeof(int64_t) * (size_t)kWarps * g.ncp);
-  L.off_bscr = take(sizeof(int64_t) * (size_t)kWarps * 32 * 8);
+  L.off_bscr = take(sizeof(int64_t) * (size_t)kWarps * kScrStride * 8);
   L.off_bshr = take(0);
   L.off_bshg = take(0);
   L.bulk_total = o;
@@ -718,13 +719,13 @@ __device__ __forceinline__ void run_reduce(const int64_t (&acc)[8], const int* g
                                            int nout, int ncp, bool accumulate = false) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int r = 0; r < 8; r++) scr[lane * 8 + r] = acc[r];
+  for (int r = 0; r < 8; r++) scr[r * kScrStride + lane] = acc[r];  // column-major, odd stride: no bank conflicts
   __syncwarp();
   for (int c = lane; c < ncp; c += 32) {
     int64_t s = 0;
     if (c < nout && c < 8 * ng) {
       const int g = c >> 3, r = c & 7;
-      for (int l = gl[g]; l < gl[g + 1]; l++) s += scr[l * 8 + r];
+      for (int l = gl[g]; l < gl[g + 1]; l++) s += scr[r * kScrStride + l];
     }
     out[c] = accumulate ? out[c] + s : s;
   }
@@ -924,7 +925,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
     int nlt[32];
     const bool fast = g.ng <= 32 && plan_lanes(g.Tc, p.W, g.KW, g.ng, nlt) >= 0 &&
                       plan_lanes(g.Tc, p.W, p.W, g.ng, nlt) >= 0 && plan_lanes(g.T, p.W, p.W, g.ng, nlt) >= 0;
-    int64_t* scr = (int64_t*)(smem + L.off_scr) + (size_t)warp * 32 * 8;
+    int64_t* scr = (int64_t*)(smem + L.off_scr) + (size_t)warp * kScrStride * 8;
     int4* shr = (int4*)(smem + L.off_lshr);
     int* shg = (int*)(smem + L.off_lshg);
     // zero-skipping schedules (zs_product) measured slower at K=500: the per-product
@@ -1229,7 +1230,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
     const LaneRun lrb = lane_run(g.T, p.W, p.W, g.ng, lane, s_gl[2]);
     int nlb[32];
     const bool bfast = g.ng <= 32 && plan_lanes(g.T, p.W, p.W, g.ng, nlb) >= 0;
-    int64_t* bscr = (int64_t*)(smem + L.off_bscr) + (size_t)warp * 32 * 8;
+    int64_t* bscr = (int64_t*)(smem + L.off_bscr) + (size_t)warp * kScrStride * 8;
     int4* bshr = (int4*)(smem + L.off_bshr);
     int* bshg = (int*)(smem + L.off_bshg);
     constexpr bool bzskip = false;
