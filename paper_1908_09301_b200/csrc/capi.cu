@@ -29,6 +29,9 @@ bool warp_supported(const Params& p);
 size_t warp_traj_smem(const Params& p);
 int warp_choose_wpb(const Params& p, size_t smem_sm, size_t optin);
 cudaError_t launch_warp_kernel(const Params& p, int wpb, cudaStream_t stream);
+bool block_supported(const Params& p);
+size_t block_smem_bytes(const Params& p);
+cudaError_t launch_block_kernel(const Params& p, cudaStream_t stream);
 }  // namespace mpt
 
 static thread_local std::string g_err;
@@ -60,7 +63,8 @@ struct mpt_plan {
   bool have_constants = false;
   unsigned long long* d_counters = nullptr;
   bool counting = false;
-  int kernel = 0;    // 1 team (rows in HBM/L2), 4 grid (all SMs), 6 mx (matrix recurrence), 7 warp (one warp per trajectory)
+  int kernel = 0;    // 1 team (rows in HBM/L2), 4 grid (all SMs), 6 mx (matrix recurrence), 7 warp (one warp per trajectory),
+                     // 8 block (one CTA per trajectory, rows in shared memory)
   int warp_wpb = 0;  // warp kernel: trajectories (warps) per CTA
   int smem_sm = 0;   // shared memory per SM
   int cluster = 1;   // CTAs per trajectory (mx), co-resident CTAs (grid)
@@ -138,6 +142,21 @@ static int choose_kernel(mpt_plan* pl, int kernel, int want) {
       return MPT_OK;
     }
     return fail(MPT_EUNSUP, "the warp kernel does not support this system/precision (W <= 34 digits, integer bilinear coefficients, rows in shared memory)");
+  }
+  // medium precision ensembles (35..58 digits): one CTA per trajectory, rows in shared memory
+  if ((kernel == 8 || (kernel == 0 && p.n_traj >= pl->nsm / 2)) && pl->have_constants && mpt::block_supported(p) &&
+      mpt::block_smem_bytes(p) <= (size_t)pl->optin) {
+    pl->kernel = 8;
+    pl->cluster = 1;
+    pl->smem_cluster = mpt::block_smem_bytes(p);
+    return MPT_OK;
+  }
+  if (kernel == 8) {
+    if (!pl->have_constants) {
+      pl->kernel = 0;
+      return MPT_OK;
+    }
+    return fail(MPT_EUNSUP, "the block kernel does not support this system/precision (W <= 58 digits, <= 2 integer-coefficient pairs, rows in shared memory)");
   }
   const int tries[] = {16, 8, 4, 2, 1};
   // the matrix-recurrence kernel (lead CTA + bulk CTAs, K table in global memory)
@@ -371,6 +390,7 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
                        : strcmp(ek, "grid") == 0 ? 4
                        : strcmp(ek, "mx") == 0   ? 6
                        : strcmp(ek, "warp") == 0 ? 7
+                       : strcmp(ek, "block") == 0 ? 8
                                                  : 0)
                     : 0;
     int want = ec ? atoi(ec) : (n_traj == 1 ? 16 : 1);
@@ -385,7 +405,8 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
 }
 
 int mpt_plan_configure(mpt_plan* pl, int kernel, int cluster) {
-  if (!pl || (kernel != 0 && kernel != 1 && kernel != 4 && kernel != 6 && kernel != 7) || cluster < 1 || cluster > 16)
+  if (!pl || (kernel != 0 && kernel != 1 && kernel != 4 && kernel != 6 && kernel != 7 && kernel != 8) || cluster < 1 ||
+      cluster > 16)
     return fail(MPT_EINVAL, "bad configuration");
   return choose_kernel(pl, kernel, cluster);
 }
@@ -427,7 +448,7 @@ int mpt_plan_info(const mpt_plan* pl, int* smem_bytes, int* k_chunk, int* thread
     k_chunk = nullptr;
   }
   if (k_chunk) *k_chunk = pl->p.kc;
-  if (threads) *threads = pl->kernel == 7 ? 32 * pl->warp_wpb : pl->p.nthreads;
+  if (threads) *threads = pl->kernel == 7 ? 32 * pl->warp_wpb : pl->kernel == 8 ? 256 : pl->p.nthreads;
   return MPT_OK;
 }
 
@@ -527,6 +548,8 @@ static int launch(mpt_plan* pl, int n_steps, int start_step, int stride, cudaStr
     CK(mpt::launch_mx_kernel(p, pl->cluster, pl->smem_cluster, stream));
   } else if (pl->kernel == 7) {
     CK(mpt::launch_warp_kernel(p, pl->warp_wpb, stream));
+  } else if (pl->kernel == 8) {
+    CK(mpt::launch_block_kernel(p, stream));
   } else {
     CK(mpt::launch_team_kernel(p, pl->smem, stream));
   }

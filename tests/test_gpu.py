@@ -151,6 +151,28 @@ def test_warp_kernel_bit_exact(gpu, K, N, steps, n_traj):
         assert np.array_equal(jets[j], FX.compute_jet(tables, fmt.frac_digits, N, states[j], **kw)), j
 
 
+@pytest.mark.parametrize("K,N,steps,n_traj", [(100, 60, 3, 3), (300, 40, 3, 2), (400, 240, 1, 3), (450, 270, 1, 2),
+                                              (470, 30, 2, 1)])
+def test_block_kernel_bit_exact(gpu, K, N, steps, n_traj):
+    """One CTA per trajectory, rows in shared memory (W <= 58 digits, every product
+    window width up to 60): records and the jet bit-exact vs the value-exact model."""
+    P = M.bits_for_digits(K)
+    ctx, system, fmt, tables = lorenz_tables(P, N)
+    base = [M.mp_from_decimal(t, ctx).as_fraction() for t in CANON_INIT]
+    states = np.stack([fmt.to_digits([b + Fraction(3 * j - 2, 10**18) for b in base]) for j in range(n_traj)])
+    with DevicePlan(tables, fmt, N, n_traj) as plan:
+        plan.configure("block", 1)
+        assert plan.info()["kernel"] == "block"
+        _, r_gpu, status = plan.integrate(states, steps, 0, 1)
+        jets = plan.compute_jet(states)
+        kw = plan.model_kwargs()
+    assert kw == {"variant": 3} and not status.any()
+    for j in sorted({0, n_traj - 1}):
+        _, r_cpu = FX.integrate(tables, fmt.frac_digits, N, P, states[j], steps, 0, 1, **kw)
+        assert np.array_equal(r_gpu[:, j], r_cpu), j
+        assert np.array_equal(jets[j], FX.compute_jet(tables, fmt.frac_digits, N, states[j], **kw)), j
+
+
 def test_random_quadratic_systems_jets_bit_exact(golden, gpu):
     for name, c in golden.items():
         if not name.startswith("random_jet"):
