@@ -213,7 +213,7 @@ def test_dropin_integrate_matches_reference(golden, gpu, name):
 
 LONG_RUNS = ("config1_k500_n200_10000", "config2_k2200_n1000_500", "config3_k4200_n3500_4",
              "config3_k4200_n3500_100")
-ERROR_BUDGET_RUNS = ("config1_k500_n200_10000", "config2_k2200_n1000_500")
+ERROR_BUDGET_RUNS = ("config1_k500_n200_10000", "config2_k2200_n1000_500", "config3_k4200_n3500_100")
 
 
 @pytest.mark.parametrize("name", LONG_RUNS)

@@ -127,8 +127,8 @@ def test_reference_error_budget_against_p64_oracle():
     """How much of d(t) is the reference's own rounding: the oracle at P bits
     against the same oracle at P + 64 bits (same inputs, same order, so the
     truncation error is shared). The declared d(t) keeps >= 2 digits of margin
-    over the reference's measured loss on configs[1] and configs[2]."""
-    for name in ("config1_k500_n200_10000", "config2_k2200_n1000_500"):
+    over the reference's measured loss on configs[1], configs[2] and configs[3]."""
+    for name in ("config1_k500_n200_10000", "config2_k2200_n1000_500", "config3_k4200_n3500_100"):
         ref, truth = _oracle_fixture(name), _oracle_fixture(name + "_p64")
         assert truth["work_prec_bits"] == ref["prec_bits"] + 64 and truth["order"] == ref["order"]
         K, tau = ref["K"], float(ref["tau"])
@@ -138,7 +138,7 @@ def test_reference_error_budget_against_p64_oracle():
             assert 0 <= lost <= guard_digits(ra["step"] * tau, ref["order"], tau) - 2, (name, ra["step"], lost)
 
 
-@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("variant", [1, 3])  # the arithmetic of the kernels that run configs[1]-like shapes (mx, warp/block)
 def test_model_is_at_least_as_accurate_as_the_reference(variant):
     """configs[1], first 1000 steps (t = 10): the device arithmetic's distance
     from the P + 64-bit oracle equals the reference's own to within one digit
