@@ -209,6 +209,10 @@ def run_reference(args, rank, world):
                                    f"bit-identical to it), OpenMP {threads} threads, 64 chunks, "
                                    f"serial threshold {threshold}"},
         "e2e": {"value": value, "unit": "taylor_steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "the reference itself is Python on gmpy2 (not installed in this image); this arm is its C/MPFR "
+                "restatement (pinned bit for bit to the unmodified reference, including this chunked plan) with "
+                "OpenMP over the reference's chunks, so it is FASTER than the reference's own loop and the GPU/"
+                "reference ratio against it is conservative",
     }
     return line
 

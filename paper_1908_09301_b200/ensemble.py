@@ -26,7 +26,7 @@ import numpy as np
 
 from .cns import AGREEMENT_EXACT, tc_from_series
 from .engine import DevicePlan, SystemTables
-from .fixed import MAX_INT_BITS, FixedFormat
+from .fixed import MAX_INT_BITS, RADIX, RADIX_BITS, FixedFormat
 from .mp import _DECIMAL_RE, PrecisionContext, RangeError, _round_scaled, bits_for_digits, mp_from_decimal
 from .systems import builtin_system
 from .taylor import checked_out_plan, exact_time
@@ -146,11 +146,75 @@ def _floor_neg_log10(num: int, den: int, pow10: list) -> int:
     return d
 
 
+def _agreement_exact(x: int, y: int, one: int, pow10: list) -> int:
+    if x == y:
+        return EXACT_CODE
+    return _floor_neg_log10(abs(x - y), max(abs(x), abs(y), one), pow10)
+
+
+def _top3(dig: np.ndarray):
+    """(mantissa, digit exponent) of the values of signed digit rows [n, W]:
+    value ~= mantissa * B^exponent from the three leading nonzero digits
+    (relative error < 2^-25); zero rows give mantissa 0."""
+    n, W = dig.shape
+    nz = dig != 0
+    top = np.where(nz.any(axis=1), W - 1 - np.argmax(nz[:, ::-1], axis=1), 2)
+    top = np.maximum(top, 2)
+    idx = np.arange(n)
+    B = float(RADIX)
+    mant = (dig[idx, top].astype(np.float64) * B + dig[idx, top - 1]) * B + dig[idx, top - 2]
+    return mant, top - 2
+
+
 def agreement_matrix(a: EnsembleRun, b: EnsembleRun) -> np.ndarray:
     """[nrec, members] agreement digits (cns.py:52; EXACT_CODE for identical
-    samples), exact integer arithmetic on the aligned fixed-point numerators."""
+    samples). The digit count floor(-log10(|x-y| / max(|x|, |y|, 1))) is
+    evaluated in floating point on the three leading digits of the aligned
+    fixed-point rows (both formats are whole radix-2^28 digits apart), and
+    recomputed in exact integer arithmetic wherever the estimate is within 1e-6
+    of an integer boundary, so the result is the exact one."""
     if not np.array_equal(a.steps, b.steps) or a.records.shape[1] != b.records.shape[1]:
         raise ValueError("runs are not sampled on the same grid / members")
+    la, lb = a.fmt.frac_digits, b.fmt.frac_digits
+    Lf = max(la, lb)
+    F = RADIX_BITS * Lf
+    one = 1 << F
+    cap = (max(a.bits, b.bits) * 30103) // 100000 + 8
+    pow10 = [10**k for k in range(cap + 2)]
+    nrec, members, dim = a.records.shape[0], a.records.shape[1], a.records.shape[2]
+    out = np.zeros((nrec, members), np.int64)
+    log10B = RADIX_BITS * np.log10(2.0)
+
+    def aligned(run, lf, r):  # digit rows on the common grid, [members*dim, Lf + 1]
+        rows = run.records[r].reshape(members * dim, -1).astype(np.int64)
+        return np.pad(rows, ((0, 0), (Lf - lf, 0)))
+
+    for r in range(nrec):
+        da, db = aligned(a, la, r), aligned(b, lb, r)
+        md, ed = _top3(da - db)
+        ma, ea = _top3(da)
+        mb, eb = _top3(db)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            lg_d = np.log10(np.abs(md)) + ed * log10B
+            lg_g = np.maximum(np.maximum(np.log10(np.abs(ma)) + ea * log10B, np.log10(np.abs(mb)) + eb * log10B), Lf * log10B)
+            est = lg_g - lg_d  # log10(max(|x|, |y|, 1) / |x - y|)
+        same = md == 0
+        est = np.where(same, 0.5, est)
+        digits = np.floor(est)
+        risky = ~same & (np.abs(est - np.round(est)) < 1e-6)
+        digits = np.where(est < 0, 0, digits).astype(np.int64)
+        digits[same] = EXACT_CODE
+        if risky.any():
+            ia = a.fmt.digits_to_ints(a.records[r].reshape(members * dim, -1)[risky])
+            ib = b.fmt.digits_to_ints(b.records[r].reshape(members * dim, -1)[risky])
+            sa, sb = RADIX_BITS * (Lf - la), RADIX_BITS * (Lf - lb)
+            digits[risky] = [_agreement_exact(x << sa, y << sb, one, pow10) for x, y in zip(ia, ib)]
+        out[r] = digits.reshape(members, dim).min(axis=1)
+    return out
+
+
+def agreement_matrix_exact(a: EnsembleRun, b: EnsembleRun) -> np.ndarray:
+    """agreement_matrix in exact integer arithmetic throughout (the checker of the fast path)."""
     fa, fb = a.fmt.frac_bits, b.fmt.frac_bits
     F = max(fa, fb)
     sa, sb = F - fa, F - fb
@@ -162,15 +226,7 @@ def agreement_matrix(a: EnsembleRun, b: EnsembleRun) -> np.ndarray:
     for r in range(nrec):
         ia, ib = a.ints(r), b.ints(r)
         for m in range(members):
-            worst = EXACT_CODE
-            for x, y in zip(ia[m], ib[m]):
-                x <<= sa
-                y <<= sb
-                if x == y:
-                    continue
-                g = max(abs(x), abs(y), one)
-                worst = min(worst, _floor_neg_log10(abs(x - y), g, pow10))
-            out[r, m] = worst
+            out[r, m] = min(_agreement_exact(x << sa, y << sb, one, pow10) for x, y in zip(ia[m], ib[m]))
     return out
 
 

@@ -274,3 +274,25 @@ def test_decimal_to_fixed_int_matches_mp_path():
             E.decimal_to_fixed_int("134217728", bits, fmt)
         with pytest.raises(ValueError):
             E.decimal_to_fixed_int("1,5", bits, fmt)
+
+
+def test_agreement_matrix_fast_path_equals_exact():
+    """The vectorised digit count (three leading digits in floating point, exact
+    fallback near integer boundaries) against the all-integer computation, on
+    random differences of every size and on exact powers of ten."""
+    rng = np.random.default_rng(11)
+    steps = list(range(6))
+    base, ver = [], []
+    for r in steps:
+        rb, rv = [], []
+        for m in range(40):
+            x = [Fraction(int(rng.integers(-10**12, 10**12)), 10 ** int(rng.integers(5, 14))) for _ in range(3)]
+            k = int(rng.integers(1, 70))
+            eps = Fraction(int(rng.integers(1, 10)) if m % 3 else 1, 10**k)  # m % 3 == 0: exactly 10^-k
+            rb.append(x)
+            rv.append([x[0] + eps * (m % 2), x[1] - eps, x[2] if m % 5 else x[2] * 0])
+        base.append(rb)
+        ver.append(rv)
+    a, b = _fake_run(300, base, steps), _fake_run(470, ver, steps)
+    assert np.array_equal(E.agreement_matrix(a, b), E.agreement_matrix_exact(a, b))
+    assert (E.agreement_matrix(a, a) == E.EXACT_CODE).all()
