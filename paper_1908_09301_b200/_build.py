@@ -17,7 +17,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
-SOURCES = ("csrc/taylor_kernel.cu", "csrc/taylor_grid.cu", "csrc/taylor_mx.cu", "csrc/taylor_warp.cu", "csrc/taylor_warp2.cu", "csrc/taylor_block.cu",
+SOURCES = ("csrc/taylor_kernel.cu", "csrc/taylor_grid.cu", "csrc/taylor_mx.cu", "csrc/taylor_warp.cu", "csrc/taylor_warp2.cu", "csrc/taylor_block.cu", "csrc/taylor_cblock.cu",
            "csrc/capi.cu")
 OUT = os.path.join(HERE, "_lib", "libmptaylor_b200.so")
 ARCH = ("-gencode", "arch=compute_100a,code=sm_100a")

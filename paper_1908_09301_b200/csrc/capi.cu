@@ -32,6 +32,10 @@ cudaError_t launch_warp_kernel(const Params& p, int wpb, cudaStream_t stream);
 bool block_supported(const Params& p);
 size_t block_smem_bytes(const Params& p);
 cudaError_t launch_block_kernel(const Params& p, cudaStream_t stream);
+bool cblock_supported(const Params& p);
+size_t cblock_smem_bytes(const Params& p, int G);
+int cblock_max_clusters(const Params& p, size_t smem, int G);
+cudaError_t launch_cblock_kernel(const Params& p, int G, size_t smem, cudaStream_t stream);
 }  // namespace mpt
 
 static thread_local std::string g_err;
@@ -64,7 +68,8 @@ struct mpt_plan {
   unsigned long long* d_counters = nullptr;
   bool counting = false;
   int kernel = 0;    // 1 team (rows in HBM/L2), 4 grid (all SMs), 6 mx (matrix recurrence), 7 warp (one warp per trajectory),
-                     // 8 block (one CTA per trajectory, rows in shared memory)
+                     // 8 block (one CTA per trajectory, rows in shared memory), 9 cblock (one cluster per trajectory,
+                     // rows in every CTA's shared memory, all-gather of partial Cauchy sums)
   int warp_wpb = 0;  // warp kernel: trajectories (warps) per CTA
   int smem_sm = 0;   // shared memory per SM
   int cluster = 1;   // CTAs per trajectory (mx), co-resident CTAs (grid)
@@ -159,6 +164,27 @@ static int choose_kernel(mpt_plan* pl, int kernel, int want) {
     return fail(MPT_EUNSUP, "the block kernel does not support this system/precision (W <= 58 digits, <= 2 integer-coefficient pairs, rows in shared memory)");
   }
   const int tries[] = {16, 8, 4, 2, 1};
+  // medium precision, few trajectories: one cluster per trajectory, rows in every CTA's shared memory
+  if (kernel == 9 && pl->have_constants &&
+      mpt::cblock_supported(p)) {
+    for (int G : tries) {
+      if (G > want || G < 2) continue;
+      const size_t s = mpt::cblock_smem_bytes(p, G);
+      if (s > (size_t)pl->optin) continue;
+      if (mpt::cblock_max_clusters(p, s, G) < 1) continue;
+      pl->kernel = 9;
+      pl->cluster = G;
+      pl->smem_cluster = s;
+      return MPT_OK;
+    }
+  }
+  if (kernel == 9) {
+    if (!pl->have_constants) {
+      pl->kernel = 0;
+      return MPT_OK;
+    }
+    return fail(MPT_EUNSUP, "the cblock kernel does not support this system/precision (W <= 93 digits, <= 2 integer-coefficient pairs, rows in shared memory)");
+  }
   // the matrix-recurrence kernel (lead CTA + bulk CTAs, K table in global memory)
   if ((kernel == 0 || kernel == 6) && pl->have_constants && mpt::mx_supported(p) && (kernel == 6 || p.n_traj == 1)) {
     for (int G : tries) {
@@ -391,6 +417,7 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
                        : strcmp(ek, "mx") == 0   ? 6
                        : strcmp(ek, "warp") == 0 ? 7
                        : strcmp(ek, "block") == 0 ? 8
+                       : strcmp(ek, "cblock") == 0 ? 9
                                                  : 0)
                     : 0;
     int want = ec ? atoi(ec) : (n_traj == 1 ? 16 : 1);
@@ -405,7 +432,7 @@ int mpt_plan_create(mpt_plan** out, int dim, int nterms, const int32_t* term_eq,
 }
 
 int mpt_plan_configure(mpt_plan* pl, int kernel, int cluster) {
-  if (!pl || (kernel != 0 && kernel != 1 && kernel != 4 && kernel != 6 && kernel != 7 && kernel != 8) || cluster < 1 ||
+  if (!pl || (kernel != 0 && kernel != 1 && kernel != 4 && kernel != 6 && kernel != 7 && kernel != 8 && kernel != 9) || cluster < 1 ||
       cluster > 16)
     return fail(MPT_EINVAL, "bad configuration");
   return choose_kernel(pl, kernel, cluster);
@@ -448,7 +475,7 @@ int mpt_plan_info(const mpt_plan* pl, int* smem_bytes, int* k_chunk, int* thread
     k_chunk = nullptr;
   }
   if (k_chunk) *k_chunk = pl->p.kc;
-  if (threads) *threads = pl->kernel == 7 ? 32 * pl->warp_wpb : pl->kernel == 8 ? 256 : pl->p.nthreads;
+  if (threads) *threads = pl->kernel == 7 ? 32 * pl->warp_wpb : pl->kernel == 8 ? 256 : pl->kernel == 9 ? 512 : pl->p.nthreads;
   return MPT_OK;
 }
 
@@ -550,6 +577,8 @@ static int launch(mpt_plan* pl, int n_steps, int start_step, int stride, cudaStr
     CK(mpt::launch_warp_kernel(p, pl->warp_wpb, stream));
   } else if (pl->kernel == 8) {
     CK(mpt::launch_block_kernel(p, stream));
+  } else if (pl->kernel == 9) {
+    CK(mpt::launch_cblock_kernel(p, pl->cluster, pl->smem_cluster, stream));
   } else {
     CK(mpt::launch_team_kernel(p, pl->smem, stream));
   }

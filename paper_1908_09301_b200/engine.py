@@ -52,7 +52,7 @@ class SystemTables:
         )
 
 
-KERNEL_NAMES = {1: "team", 4: "grid", 6: "mx", 7: "warp", 8: "block"}  # include/mptaylor_b200.h mpt_plan_configure
+KERNEL_NAMES = {1: "team", 4: "grid", 6: "mx", 7: "warp", 8: "block", 9: "cblock"}  # include/mptaylor_b200.h mpt_plan_configure
 
 
 def _p(a: np.ndarray):
@@ -128,7 +128,7 @@ class DevicePlan:
         _native.check(self.lib.mpt_plan_kernel(self.h, ctypes.byref(kern), ctypes.byref(cl)))
         if kern.value == 6:
             return {"variant": 1, "bulk": cl.value - 1}
-        if kern.value in (7, 8):
+        if kern.value in (7, 8, 9):
             return {"variant": 3}
         return {"variant": 0}
 
