@@ -68,11 +68,17 @@ int mpt_plan_destroy(mpt_plan *plan);
  *   W <= 34 digits, integer bilinear coefficients, rows fit shared memory
  *                      -> 7 warp kernel (one warp per trajectory; ensembles and small
  *                         single trajectories)
+ *   ensembles (>= SMs / 2 trajectories) at 35..58 digits
+ *                      -> 8 block kernel (one CTA per trajectory, rows in shared memory)
  *   one trajectory     -> 6 mx (matrix recurrence on a 16-CTA cluster, W <= 120 digits),
  *                         else 4 grid kernel (one trajectory on every SM, rows in L2)
  *   ensembles          -> 1 team kernel (one CTA per trajectory, rows in HBM/L2)
- * kernel: 0 auto, 1 team, 4 grid, 6 mx, 7 warp; cluster: CTAs per trajectory (2..16) for mx.
- * Environment overrides at plan creation: MPT_KERNEL=team|grid|mx|warp, MPT_CLUSTER=G,
+ *   on request         -> 9 cblock kernel (one cluster per trajectory, every CTA keeps all rows
+ *                         in shared memory, partial Cauchy sums all-gathered through DSMEM;
+ *                         W <= 93 digits)
+ * kernel: 0 auto, 1 team, 4 grid, 6 mx, 7 warp, 8 block, 9 cblock; cluster: CTAs per trajectory
+ * (2..16) for mx and cblock.
+ * Environment overrides at plan creation: MPT_KERNEL=team|grid|mx|warp|block|cblock, MPT_CLUSTER=G,
  * MPT_TEAM_MB=1|2|4|8 (team kernel CTAs per SM; default 8 (64 threads) when n_traj >= 8 x SMs
  * and W <= 20, 4 (128 threads) when n_traj >= 4 x SMs and W <= 64, 2 when n_traj >= 2 x SMs). */
 int mpt_plan_configure(mpt_plan *plan, int kernel, int cluster);

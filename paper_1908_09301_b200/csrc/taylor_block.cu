@@ -4,7 +4,7 @@
 // trajectory fill most of an SM's shared memory.
 //
 // Same arithmetic as the warp kernel (oracle/fixmodel.c jet_wp, variant 3:
-// value-exact sd roundings, direct per-order recurrence; reference
+// value-exact roundings (kept in semi-normal digits inside the kernel, canonical sd digits on output), direct per-order recurrence; reference
 // taylor.py:117 _jet_rows, reduction.py:149 convolve, taylor.py:168
 // horner_eval) and the same building blocks (taylor_warp_impl.cuh): top-aligned
 // NU-digit windows, a fully unrolled register triangle per lane, one fold, a
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_block_kernel(const __grid_
         const int d = lane * MC + j - 2;
         v[0][j] = (d >= 0 && d < W) ? st[m * p.RS + d] : 0;
       }
-      ovf |= wp::warp_sd<MC, false, 1>(v, 1, W, e0);
+      ovf |= wp::warp_bal<MC, false, 1>(v, 1, W, e0);
       const int z = wp::lead_zeros<MC>(e0[0], Lf);
 #pragma unroll
       for (int j = 0; j < MC; j++) {
@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_block_kernel(const __grid_
           }
         }
         int32_t ureg[1][MC];
-        ovf |= wp::warp_sd<MC, true, 1>(U, 1, W, ureg);
+        ovf |= wp::warp_bal<MC, true, 1>(U, 1, W, ureg);
         int32_t* ub = ubuf + (size_t)m * (W + 4);
 #pragma unroll
         for (int j = 0; j < MC; j++) {
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_block_kernel(const __grid_
           }
         }
         int32_t rowreg[1][MC];
-        ovf |= wp::warp_sd<MC, true, 1>(x, 1, W, rowreg);
+        ovf |= wp::warp_bal<MC, true, 1>(x, 1, W, rowreg);
         const int z2 = wp::lead_zeros<MC>(rowreg[0], Lf);
 #pragma unroll
         for (int j = 0; j < MC; j++) {
@@ -398,8 +398,23 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_block_kernel(const __grid_
 
     if (p.write_coef) {
       int32_t* gcoef = p.coef + (size_t)traj * D * N1 * p.RS;
-      for (int r = warp; r < D * N1; r += kWarps)
-        for (int d = lane; d < p.RS; d += 32) gcoef[(size_t)r * p.RS + d] = d < W ? rows[(size_t)r * L.stride + d] : 0;
+      // rows leave the kernel in canonical form: sd of the value the semi-normal digits hold
+#pragma unroll 1
+      for (int r = warp; r < D * N1; r += kWarps) {
+        int64_t cv[1][MC];
+        int32_t ce[1][MC];
+#pragma unroll
+        for (int j = 0; j < MC; j++) {
+          const int d = lane * MC + j - 2;
+          cv[0][j] = (d >= 0 && d < W) ? rows[(size_t)r * L.stride + d] : 0;
+        }
+        wp::warp_sd<MC, false, 1>(cv, 1, W, ce);
+#pragma unroll
+        for (int j = 0; j < MC; j++) {
+          const int d = lane * MC + j - 2;
+          if (d >= 0 && d < p.RS) gcoef[(size_t)r * p.RS + d] = d < W ? ce[0][j] : 0;
+        }
+      }
     }
     // ---- state = RN_P(sum of the rows)
     if (target) {

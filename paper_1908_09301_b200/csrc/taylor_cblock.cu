@@ -25,13 +25,15 @@
 //        k slots of a warp are summed with shuffles. Meanwhile the top warps
 //        compute the non-integer linear product, stage C_i and the zero-digit
 //        minimum of the next order's old terms.
+//        Three side warps prepare everything of U^m that only needs row i
+//        (constant, integer and non-integer linear terms) as pre[m].
 //   P1b  column sums over this CTA's warps; every value is PUSHED into the receive
 //        slot [i & 1][g] of every CTA (st.shared::cluster)
 //   --   cluster barrier (release / acquire)
-//   P2   tot[q][element] = sum of the G received partial sums (local reads)
-//   P3a  warp m: U^m = rndb(cst + lin a~_i + sum_q pm tot[q] + linear product)
-//   P3b  12 warps: U^m (x) C_i, four p-ranges per variable
-//   P3c  warp m: new row = rndb(sum of the four partial vectors), row sum
+//   P3a  warp m: U^m = rndb(pre[m] + sum_q pm[q] sum_g recv[g][q])   (local reads)
+//   P3b  U^m (x) C_i in chunks of 16 digits of U, one warp per (m, chunk): operands
+//        in registers, fully unrolled
+//   P3c  warp m: new row = rndb(sum of the chunk vectors), row sum
 // The receive slots are double-buffered by the order's parity, so one cluster
 // barrier per order suffices.
 #include <cooperative_groups.h>
@@ -49,14 +51,16 @@ constexpr int kThreads = 32 * kWarps;
 constexpr int kLo = 6;       // zero digits below digit 0 of every row (window reads reach -5)
 constexpr int MC = 3;        // columns per lane of the target warps (Lf + 4 <= 96)
 constexpr int DT = 3;        // variables, one target warp each
-constexpr int kParts = 4;    // warps per U (x) C_i product and per linear product
 constexpr int kCols = 32 * MC;
 constexpr int kMaxQ = 2;     // product pairs
 constexpr int kUnit = 10;    // int64 per unit: two windows of 5 folded values
+constexpr int kPC = 16;      // digits of U per chunk of the U (x) C_i product
+constexpr int kCLo = 20;     // zero digits below digit 0 of the staged C_i
+constexpr int kSumWarp0 = 8; // first warp of the P1b threads
 
 struct Layout {
-  int ncols, stride, nrows, bw, sw, nbig, nE, h2p;
-  size_t off_rows, off_zt, off_cbuf, off_lbuf, off_ubuf, off_linp, off_tot, off_nscr, off_st, off_scr, off_recv, total;
+  int ncols, stride, nrows, bw, cw, sw, nbig, nE, h2p, nch, ustride;
+  size_t off_rows, off_zt, off_cbuf, off_lbuf, off_ubuf, off_pre, off_nscr, off_st, off_scr, off_recv, total;
 };
 
 __host__ __device__ inline int pow2_ge(int x) {
@@ -71,29 +75,32 @@ __host__ __device__ inline Layout make_layout(const Params& p, int G) {
   L.stride = (kLo + p.W) | 1;  // odd: lanes reading consecutive rows hit different banks
   L.nrows = p.D * (p.N + 1);
   L.bw = 4 + p.W + p.Lf + 4;
+  L.cw = kCLo + 2 * p.Lf + 12;
   L.sw = p.W + 3;
   L.nbig = wp::n_big_lin(p);
   const int Hmax = (p.Lf + 3 + 3) / 4;
   L.nE = 4 * Hmax + 1;                 // elements (columns) of one pair's partial sums
   L.h2p = pow2_ge((Hmax + 1) / 2);     // lanes per k slot at the widest window
+  L.nch = (p.W + kPC - 1) / kPC;
+  L.ustride = kPC * L.nch + 4;
   size_t o = 0;
   auto take = [&](size_t bytes) {
     size_t r = o;
     o += (bytes + 15) / 16 * 16;
     return r;
   };
+  take(64);  // the operand prefetch of win_mac may read a few words below row 0
   L.off_rows = take(sizeof(int32_t) * ((size_t)L.nrows * L.stride + 2 * kLo));
   L.off_zt = take((size_t)L.nrows);
-  L.off_cbuf = take(sizeof(int32_t) * (size_t)L.bw);
+  L.off_cbuf = take(sizeof(int32_t) * (size_t)L.cw);
   L.off_lbuf = take(sizeof(int32_t) * (size_t)L.bw * (L.nbig > 0 ? L.nbig : 1));
-  L.off_ubuf = take(sizeof(int32_t) * (size_t)DT * (p.W + 4));
-  L.off_linp = take(sizeof(int64_t) * (size_t)DT * kParts * kCols);
-  L.off_tot = take(sizeof(int64_t) * kMaxQ * L.nE);
+  L.off_ubuf = take(sizeof(int32_t) * (size_t)DT * L.ustride);
+  L.off_pre = take(sizeof(int64_t) * (size_t)DT * kCols);
   L.off_nscr = take(sizeof(int64_t) * (size_t)p.D * L.sw);
   L.off_st = take(sizeof(int32_t) * (size_t)p.D * p.RS + sizeof(int2) * kMaxD);
-  // unit scratch [warp][window pair][10]; the partial products of P3b reuse it
+  // unit scratch [warp][window pair][10]; the chunk vectors of P3b reuse it
   const size_t scr1 = sizeof(int64_t) * (size_t)kWarps * L.h2p * kUnit;
-  const size_t scr2 = sizeof(int64_t) * (size_t)DT * kParts * kCols;
+  const size_t scr2 = sizeof(int64_t) * (size_t)DT * L.nch * kCols;
   L.off_scr = take(scr1 > scr2 ? scr1 : scr2);
   L.off_recv = take(sizeof(int64_t) * 2 * (size_t)G * kMaxQ * L.nE);
   L.total = o;
@@ -109,29 +116,41 @@ __device__ __forceinline__ void win_mac(const int32_t* ap, const int32_t* bp, in
   int64_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
   const int32_t* bq = bp - r0;  // bq[u - j] = b'[r0 + j - u]
   int32_t b0 = bq[-3], b1 = bq[-2], b2 = bq[-1], b3;
+  // operands of the next iteration are loaded before this iteration's products
+  int32_t a0 = ap[0], a1 = ap[-1], a2 = ap[-2], a3 = ap[-3];
+  int32_t n0 = bq[0], n1 = bq[1], n2 = bq[2], n3 = bq[3];
 #pragma unroll 1
   for (int u = 0; u < r0 + 4; u += 4) {
-    const int32_t a0 = ap[-u], a1 = ap[-u - 1], a2 = ap[-u - 2], a3 = ap[-u - 3];
-    b3 = bq[u];
-    c0 = madw(a0, b3, c0);
-    c1 = madw(a0, b2, c1);
-    c2 = madw(a0, b1, c2);
-    c3 = madw(a0, b0, c3);
-    b0 = bq[u + 1];
-    c0 = madw(a1, b0, c0);
-    c1 = madw(a1, b3, c1);
-    c2 = madw(a1, b2, c2);
-    c3 = madw(a1, b1, c3);
-    b1 = bq[u + 2];
-    c0 = madw(a2, b1, c0);
-    c1 = madw(a2, b0, c1);
-    c2 = madw(a2, b3, c2);
-    c3 = madw(a2, b2, c3);
-    b2 = bq[u + 3];
-    c0 = madw(a3, b2, c0);
-    c1 = madw(a3, b1, c1);
-    c2 = madw(a3, b0, c2);
-    c3 = madw(a3, b3, c3);
+    const int32_t x0 = a0, x1 = a1, x2 = a2, x3 = a3;
+    const int32_t y0 = n0, y1 = n1, y2 = n2, y3 = n3;
+    a0 = ap[-u - 4];
+    a1 = ap[-u - 5];
+    a2 = ap[-u - 6];
+    a3 = ap[-u - 7];
+    n0 = bq[u + 4];
+    n1 = bq[u + 5];
+    n2 = bq[u + 6];
+    n3 = bq[u + 7];
+    b3 = y0;
+    c0 = madw(x0, b3, c0);
+    c1 = madw(x0, b2, c1);
+    c2 = madw(x0, b1, c2);
+    c3 = madw(x0, b0, c3);
+    b0 = y1;
+    c0 = madw(x1, b0, c0);
+    c1 = madw(x1, b3, c1);
+    c2 = madw(x1, b2, c2);
+    c3 = madw(x1, b1, c3);
+    b1 = y2;
+    c0 = madw(x2, b1, c0);
+    c1 = madw(x2, b0, c1);
+    c2 = madw(x2, b3, c2);
+    c3 = madw(x2, b2, c3);
+    b2 = y3;
+    c0 = madw(x3, b2, c0);
+    c1 = madw(x3, b1, c1);
+    c2 = madw(x3, b0, c2);
+    c3 = madw(x3, b3, c3);
   }
   if (r0 + 0 >= nu) c0 = 0;
   if (r0 + 1 >= nu) c1 = 0;
@@ -144,8 +163,8 @@ __device__ __forceinline__ void win_mac(const int32_t* ap, const int32_t* bp, in
   o[4] += c3 & kMask;
 }
 
-// one out-of-line copy of the value-exact rounding for all three call sites
-// (instruction-cache footprint): columns lane*3 + j in, digits (column - 2) out
+// one out-of-line copy of the rounding for all three call sites (instruction-cache
+// footprint): columns lane*3 + j in, semi-normal digits (column - 2) of the exact value out
 struct Sd3 {
   int32_t e0, e1, e2;
   int ovf;
@@ -154,7 +173,7 @@ __device__ __noinline__ Sd3 sd3(int64_t v0, int64_t v1, int64_t v2, int half, in
   int64_t v[1][MC] = {{v0, v1, v2}};
   if (half && (threadIdx.x & 31) == 0) v[0][1] += kRadix / 2;  // column 1: the rounding half
   int32_t e[1][MC];
-  const bool ovf = wp::warp_sd<MC, false, 1>(v, 1, Wout, e);
+  const bool ovf = wp::warp_bal<MC, false, 1>(v, 1, Wout, e);
   Sd3 r;
   r.e0 = e[0][0];
   r.e1 = e[0][1];
@@ -182,11 +201,10 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cblock_kernel(const __grid
   const Layout L = make_layout(p, G);
   int32_t* rows = (int32_t*)(smem + L.off_rows) + kLo;
   uint8_t* zt = (uint8_t*)(smem + L.off_zt);
-  int32_t* cbuf = (int32_t*)(smem + L.off_cbuf) + 4;
+  int32_t* cbuf = (int32_t*)(smem + L.off_cbuf) + kCLo;
   int32_t* lbuf = (int32_t*)(smem + L.off_lbuf) + 4;
   int32_t* ubuf = (int32_t*)(smem + L.off_ubuf);
-  int64_t* linp = (int64_t*)(smem + L.off_linp);
-  int64_t* tot = (int64_t*)(smem + L.off_tot);
+  int64_t* pre = (int64_t*)(smem + L.off_pre);
   int64_t* nscr = (int64_t*)(smem + L.off_nscr);
   int32_t* st = (int32_t*)(smem + L.off_st);
   int2* stinfo = (int2*)(st + p.D * p.RS);
@@ -196,6 +214,8 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cblock_kernel(const __grid
   __shared__ int s_ovf, s_zpre[2];
   const int D = p.D, N = p.N, N1 = p.N + 1, Lf = p.Lf, W = p.W, ncols = L.ncols, NP = p.NP;
   const int T = Lf - 2, Tc = Lf + p.sc - 2, stride = L.stride, nE = L.nE, rowlen = kMaxQ * L.nE;
+  const int nch = L.nch, ustride = L.ustride;
+  const float rG = 1.0f / (float)G;
 
   for (int w = tid; w < (int)(L.total / 4); w += kThreads) ((int32_t*)smem)[w] = 0;
   if (tid == 0) {
@@ -218,20 +238,10 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cblock_kernel(const __grid
   cluster_arrive();
   cluster_wait();
 
-  // target role: warp m < D owns variable m
+  // target role: warp m < D owns variable m (roundings)
   const int m = warp;
   const bool target = warp < D;
-  bool okc[MC];
-  int32_t cstreg[MC];
-  int pm[kMaxQ], linint[DT];
-  bool hasbig = false;
-#pragma unroll
-  for (int j = 0; j < MC; j++) {
-    const int c = lane * MC + j;
-    okc[j] = c < ncols;
-    const int d = c - 2;
-    cstreg[j] = (target && d >= 0 && d < W) ? p.cst[(size_t)m * p.RS + d] : 0;
-  }
+  int pm[kMaxQ];
 #pragma unroll
   for (int q = 0; q < kMaxQ; q++) {
     int s = 0;
@@ -239,40 +249,63 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cblock_kernel(const __grid
       if (target && p.tpair[t] == q && p.teq[t] == m) s += p.tq_int[t];
     pm[q] = s;
   }
+  // side role (P1): warp 15 - e prepares pre[e] (everything of U^e that only needs row i);
+  // warp 15 also stages C_i and the zero-digit minimum of the next order's old terms
+  const int eq = (warp >= kWarps - D) ? kWarps - 1 - warp : -1;
+  bool okc[MC];
+  int32_t cstreg[MC];
+  int linint[DT];
+  unsigned bigmask = 0;
+  int bigslot[DT];
 #pragma unroll
-  for (int t = 0; t < DT; t++) {
-    linint[t] = (target && t < D && p.lin_small[m * D + t]) ? p.lin_int[m * D + t] : 0;
-    if (target && t < D && !p.lin_small[m * D + t]) hasbig = true;
+  for (int j = 0; j < MC; j++) {
+    const int c = lane * MC + j;
+    okc[j] = c < ncols;
+    const int d = c - 2;
+    cstreg[j] = (eq >= 0 && d >= 0 && d < W) ? p.cst[(size_t)eq * p.RS + d] : 0;
   }
-  // product role (P3b): warp = pm_ * kParts + ppart
-  const int pm_ = warp / kParts, ppart = warp % kParts;
-  const int Wq = (W + kParts - 1) / kParts;
-  // unit role (P1): warps alternate between the pairs
-  const int uq = warp % (NP > 0 ? NP : 1), uwi = warp / (NP > 0 ? NP : 1);
-  const int nwq = (kWarps - uq + NP - 1) / (NP > 0 ? NP : 1);  // warps of pair uq
-  const int uva = NP > 0 ? p.pj[uq] : 0, uvb = NP > 0 ? p.pk[uq] : 0;
-  // side role (P1): linear-product job (equation with a non-integer coefficient, p-range) of warps 14, 13, ...
-  const int jobw = kWarps - 2 - warp;
-  int job_m = -1;
   {
-    int nb = 0;
-    for (int mm = 0; mm < D; mm++) {
-      bool big = false;
-      for (int t = 0; t < D; t++) big |= !p.lin_small[mm * D + t];
-      if (big) {
-        if (jobw >= 0 && jobw / kParts == nb) job_m = mm;
-        nb++;
-      }
+    int slot = 0;
+    for (int e = 0; e < D * D; e++) {
+      const int mm = e / D, jv = e % D;
+      const bool big = !p.lin_small[e];
+#pragma unroll
+      for (int t = 0; t < DT; t++)
+        if (eq >= 0 && mm == eq && jv == t) {
+          linint[t] = big ? 0 : p.lin_int[e];
+          bigslot[t] = slot;
+          if (big) bigmask |= 1u << t;
+        }
+      if (big) slot++;
     }
+#pragma unroll
+    for (int t = 0; t < DT; t++)
+      if (eq < 0 || t >= D) {
+        linint[t] = 0;
+        bigslot[t] = 0;
+      }
   }
+  // unit role (P1): warps alternate between the pairs
+  const int npd = NP > 0 ? NP : 1;
+  const int uq = warp % npd, uwi = warp / npd;
+  const int nwq = (kWarps - uq + npd - 1) / npd;  // warps of pair uq
+  const int urowa = (NP > 0 ? p.pj[uq] : 0) * N1, urowb = (NP > 0 ? p.pk[uq] : 0) * N1;
+  int zra[kMaxQ], zrb[kMaxQ];
+#pragma unroll
+  for (int q = 0; q < kMaxQ; q++) {
+    zra[q] = q < NP ? p.pj[q] * N1 : 0;
+    zrb[q] = q < NP ? p.pk[q] * N1 : 0;
+  }
+  // sum role (P1b): threads 256 .. 256 + NP * EH
+  const int stid = tid - 32 * kSumWarp0;
 
   MacCount mcount;
   MacCount* mc = p.counters ? &mcount : nullptr;
   bool ovf = false;
   int64_t ssum[MC];  // target warps: running sum of the rows of variable m
 
-  // development only (MPT_DEBUG): clock64 timestamps of rank 0, warps 0 / 5 / 15, first step
-  const int dbg_w = warp == 0 ? 0 : warp == 5 ? 1 : warp == kWarps - 1 ? 2 : -1;
+  // development only (MPT_DEBUG): clock64 timestamps of rank 0, warps 0 / 8 / 13, first step
+  const int dbg_w = warp == 0 ? 0 : warp == kSumWarp0 ? 1 : warp == kWarps - 3 ? 2 : -1;
   const bool dbg_on = p.dbg && g == 0 && lane == 0 && dbg_w >= 0 && traj == 0;
 #define CB_TS(i_, k_)                                                                                       \
   do {                                                                                                      \
@@ -310,74 +343,78 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cblock_kernel(const __grid
 #pragma unroll
       for (int q = 0; q < kMaxQ; q++)
         if (q < NP) {
-          zmin = min(zmin, (int)zt[p.pj[q] * N1 + i] + (int)zt[p.pk[q] * N1]);
-          zmin = min(zmin, (int)zt[p.pj[q] * N1] + (int)zt[p.pk[q] * N1 + i]);
+          zmin = min(zmin, (int)zt[zra[q] + i] + (int)zt[zrb[q]]);
+          zmin = min(zmin, (int)zt[zra[q]] + (int)zt[zrb[q] + i]);
         }
       const int nu = NP > 0 ? Lf + 3 - zmin : 0, ctop = Lf + 2 - zmin;
       const int H = (nu + 3) >> 2, H2 = (H + 1) >> 1;
-      const int EH = 4 * H + 1;                       // elements in flight this order (per pair)
-      const int kblk = (i + G) / G;                   // ceil((i + 1) / G): k block of one CTA
+      const int EH = 4 * H + 1;                              // elements in flight this order (per pair)
+      const int kblk = (int)(((float)(i + G) + 0.5f) * rG);  // ceil((i + 1) / G): k block of one CTA
       const int k0 = g * kblk, nk = max(0, min(kblk, i + 1 - k0));
       const int par = i & 1;
+      const int h2p = H2 <= 1 ? 1 : H2 <= 2 ? 2 : H2 <= 4 ? 4 : H2 <= 8 ? 8 : 16;
+      const int cw = 32 / h2p;  // k slots per warp
       CB_TS(i, 1);
 
-      // ---- side jobs on the top warps: C_i, next order's zero-digit minimum, the linear products
-      if (warp == kWarps - 1) {
-        for (int d = lane; d < W; d += 32) cbuf[d] = __ldg(p.ctab + (size_t)i * p.RS + d);
-        // old terms of order i + 1: k = 1 .. i (rows <= i)
-        int z = 255;
-        for (int k = 1 + lane; k <= i; k += 32)
+      // ---- side warps: C_i, next order's zero-digit minimum, pre[eq]
+      if (eq >= 0) {
+        if (eq == 0) {
+          for (int d = lane; d < W; d += 32) cbuf[d] = __ldg(p.ctab + (size_t)i * p.RS + d);
+          // old terms of order i + 1: k = 1 .. i (rows <= i)
+          int z = 255;
+          for (int k = 1 + lane; k <= i; k += 32)
 #pragma unroll
-          for (int q = 0; q < kMaxQ; q++)
-            if (q < NP) z = min(z, (int)zt[p.pj[q] * N1 + i + 1 - k] + (int)zt[p.pk[q] * N1 + k]);
-        z = __reduce_min_sync(full, z);
-        if (lane == 0) s_zpre[(i + 1) & 1] = z;
-      } else if (job_m >= 0) {
-        const int jm = job_m, pt = jobw % kParts;
-        bool any = false;
-        int64_t x[MC];
+            for (int q = 0; q < kMaxQ; q++)
+              if (q < NP) z = min(z, (int)zt[zra[q] + i + 1 - k] + (int)zt[zrb[q] + k]);
+          z = __reduce_min_sync(full, z);
+          if (lane == 0) s_zpre[(i + 1) & 1] = z;
+        }
+        if (eq < D) {
+          int64_t x[MC];
 #pragma unroll
-        for (int j = 0; j < MC; j++) x[j] = 0;
-        int slot = 0;
-        for (int e = 0; e < D * D; e++) {
-          if (p.lin_small[e]) continue;
-          if (e / D == jm) {
-            any = true;
-            const int jv = e % D;
-            const int32_t* ar = rows + (jv * N1 + i) * stride;
-            const int wa = W - zt[jv * N1 + i];  // digits above are zero
-            const int wq = (wa + kParts - 1) / kParts;
-            const int p0 = pt * wq, p1 = min(wa, p0 + wq);
-            const int32_t* lb[MC];
+          for (int j = 0; j < MC; j++) {
+            const int d = lane * MC + j - 2;
+            int64_t s = i == 0 ? (int64_t)cstreg[j] : 0;
+            if (d >= 0 && d < W) {
 #pragma unroll
-            for (int j = 0; j < MC; j++) lb[j] = lbuf + slot * L.bw + (okc[j] ? lane * MC + j + T : -4);
-#pragma unroll 4
-            for (int pp = p0; pp < p1; pp++) {
-              const int32_t a = ar[pp];
-#pragma unroll
-              for (int j = 0; j < MC; j++) x[j] = madw(a, lb[j][okc[j] ? -pp : 0], x[j]);
+              for (int t = 0; t < DT; t++)
+                if (linint[t] != 0) s += (int64_t)linint[t] * rows[(t * N1 + i) * stride + d];
             }
-            if (mc && g == 0 && p1 > p0) {
-              mc->executed += (unsigned long long)(p1 - p0);
-              mc->useful += (unsigned long long)(p1 - p0) / 2 + 1;
+            x[j] = s;
+          }
+          if (bigmask) {
+#pragma unroll
+            for (int t = 0; t < DT; t++) {
+              if (bigmask & (1u << t)) {
+                // tprod(lin[eq][t], a~_i^t): row digits broadcast from shared memory
+                const int32_t* ar = rows + (t * N1 + i) * stride;
+                const int wa = W - zt[t * N1 + i];  // digits above are zero
+                const int32_t* lb[MC];
+#pragma unroll
+                for (int j = 0; j < MC; j++) lb[j] = lbuf + bigslot[t] * L.bw + (okc[j] ? lane * MC + j + T : -4);
+#pragma unroll 4
+                for (int pp = 0; pp < wa; pp++) {
+                  const int32_t a = ar[pp];
+#pragma unroll
+                  for (int j = 0; j < MC; j++) x[j] = madw(a, lb[j][okc[j] ? -pp : 0], x[j]);
+                }
+                if (mc && g == 0) {
+                  mc->executed += (unsigned long long)wa;
+                  mc->useful += (unsigned long long)wa / 2 + 1;
+                }
+              }
             }
           }
-          slot++;
-        }
-        if (any) {
 #pragma unroll
-          for (int j = 0; j < MC; j++) linp[(jm * kParts + pt) * kCols + lane * MC + j] = x[j];
+          for (int j = 0; j < MC; j++) pre[eq * kCols + lane * MC + j] = x[j];
         }
       }
       CB_TS(i, 2);
 
       if (nu > 0) {
         // ---- P1: this CTA's share of the Cauchy sums; lane = (k slot, window pair)
-        const int h2p = H2 <= 1 ? 1 : H2 <= 2 ? 2 : H2 <= 4 ? 4 : H2 <= 8 ? 8 : 16;
-        const int cw = 32 / h2p;  // k slots per warp
         const int hp = lane & (h2p - 1), cs = lane / h2p;
-        const bool uwarp = uwi * cw < nk && uq < NP;
-        if (uwarp) {
+        if (uwi * cw < nk && uq < NP) {
           int64_t o[kUnit];
 #pragma unroll
           for (int t = 0; t < kUnit; t++) o[t] = 0;
@@ -385,7 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cblock_kernel(const __grid
             const int h2 = H - 1 - hp;
             for (int kk = uwi * cw + cs; kk < nk; kk += nwq * cw) {
               const int k = k0 + kk;
-              const int ra = uva * N1 + i - k, rb = uvb * N1 + k;
+              const int ra = urowa + i - k, rb = urowb + k;
               const int za = zt[ra], zb = zt[rb];
               const int sb = min(zb, zmin), sa = zmin - sb;
               const int32_t* ap = rows + ra * stride + Lf - sa;
@@ -398,6 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cblock_kernel(const __grid
               }
             }
           }
+          CB_TS(i, 3);
           // sum the k slots of the warp
           for (int sft = h2p; sft < 32; sft <<= 1) {
 #pragma unroll
@@ -409,14 +447,14 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cblock_kernel(const __grid
             for (int t = 0; t < kUnit; t++) dst[t] = o[t];
           }
         }
-        CB_TS(i, 3);
-        __syncthreads();  // [S1] warp sums are in scratch
-        CB_TS(i, 4);
-        // ---- P1b: element sums over the warps of a pair, pushed to every CTA's receive slot
-        if (tid < NP * EH) {
-          const int q = tid >= EH ? 1 : 0, e = tid - q * EH, r = e - 1;
-          const int nwa = min((kWarps - q + NP - 1) / NP, (nk + cw - 1) / cw);  // active warps of pair q
-          int o1 = -1, o2 = -1;  // offsets of the two contributions inside a warp's scratch
+        // sum threads: where this element's two contributions sit inside a warp's scratch
+        int sq = 0, se = 0, o1 = -1, o2 = -1, nwa = 0;
+        const bool summer = stid >= 0 && stid < NP * EH;
+        if (summer) {
+          sq = stid >= EH ? 1 : 0;
+          se = stid - sq * EH;
+          const int r = se - 1;
+          nwa = min((kWarps - sq + npd - 1) / npd, (nk + cw - 1) / cw);  // active warps of pair sq
           if (r >= 0) {
             const int h = r >> 2;
             o1 = (h < H2 ? h : H - 1 - h) * kUnit + (h < H2 ? 0 : 5) + 1 + (r & 3);
@@ -425,62 +463,63 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cblock_kernel(const __grid
             const int h = (r + 1) >> 2;
             o2 = (h < H2 ? h : H - 1 - h) * kUnit + (h < H2 ? 0 : 5);
           }
+        }
+        CB_TS(i, 4);
+        __syncthreads();  // [S1] warp sums are in scratch
+        // ---- P1b: element sums over the warps of a pair, pushed to every CTA's receive slot
+        if (summer) {
           int64_t osum = 0;
           for (int wi = 0; wi < nwa; wi++) {
-            const int64_t* base = scr + ((wi * NP + q) * L.h2p) * kUnit;
+            const int64_t* base = scr + ((wi * npd + sq) * L.h2p) * kUnit;
             if (o1 >= 0) osum += base[o1];
             if (o2 >= 0) osum += base[o2];
           }
-          const uint32_t la = smem_u32(recv + (par * G + g) * rowlen + q * nE + e);
+          const uint32_t la = smem_u32(recv + (par * G + g) * rowlen + sq * nE + se);
           for (int rk = 0; rk < G; rk++) st_remote64(la, rk, osum);
         }
         CB_TS(i, 5);
         cluster_arrive();
         cluster_wait();
-        CB_TS(i, 6);
-        // ---- P2: totals from the G receive slots
-        if (tid < NP * EH) {
-          const int q = tid >= EH ? 1 : 0, e = tid - q * EH;
-          const int64_t* src = recv + (par * G) * rowlen + q * nE + e;
-          int64_t s = 0;
-          for (int rk = 0; rk < G; rk++) s += src[rk * rowlen];
-          tot[q * nE + e] = s;
-        }
+      } else {
+        __syncthreads();
       }
-      CB_TS(i, 7);
-      __syncthreads();  // [S2] tot, linp, C_i are in shared memory
-      CB_TS(i, 8);
+      CB_TS(i, 6);
 
       // ---- P3a: warp m assembles and rounds U^m
       if (target) {
         int64_t U[MC];
 #pragma unroll
-        for (int j = 0; j < MC; j++) {
-          const int c = lane * MC + j, d = c - 2;
-          int64_t s = i == 0 ? (int64_t)cstreg[j] : 0;
-          if (d >= 0 && d < W) {
+        for (int j = 0; j < MC; j++) U[j] = pre[m * kCols + lane * MC + j];
+        if (nu > 0) {
 #pragma unroll
-            for (int t = 0; t < DT; t++)
-              if (linint[t] != 0) s += (int64_t)linint[t] * rows[(t * N1 + i) * stride + d];
-          }
-          if (nu > 0) {
-            const int r = ctop - c;
-            if (r >= -1 && r < nu) {
+          for (int q = 0; q < kMaxQ; q++) {
+            if (pm[q] != 0) {
+              int64_t acc[MC];
+              const int64_t* src[MC];
 #pragma unroll
-              for (int q = 0; q < kMaxQ; q++)
-                if (pm[q] != 0) s += (int64_t)pm[q] * tot[q * nE + r + 1];
+              for (int j = 0; j < MC; j++) {
+                const int r = ctop - (lane * MC + j);
+                const bool ok = r >= -1 && r < nu;
+                acc[j] = 0;
+                // invalid columns read element 0 of an all-zero slot region (never pushed): offset nE - 1 + ...
+                src[j] = ok ? recv + (par * G) * rowlen + q * nE + r + 1 : nullptr;
+              }
+#pragma unroll 4
+              for (int rk = 0; rk < G; rk++) {
+#pragma unroll
+                for (int j = 0; j < MC; j++)
+                  if (src[j]) acc[j] += src[j][rk * rowlen];
+              }
+#pragma unroll
+              for (int j = 0; j < MC; j++) U[j] += (int64_t)pm[q] * acc[j];
             }
           }
-          if (hasbig) {
-#pragma unroll
-            for (int pt = 0; pt < kParts; pt++) s += linp[(m * kParts + pt) * kCols + c];
-          }
-          U[j] = s;
         }
+        CB_TS(i, 7);
         const Sd3 r = sd3(U[0], U[1], U[2], 1, W);
         ovf |= r.ovf != 0;
         const int32_t ureg[MC] = {r.e0, r.e1, r.e2};
-        int32_t* ub = ubuf + m * (W + 4);
+        int32_t* ub = ubuf + m * ustride;
 #pragma unroll
         for (int j = 0; j < MC; j++) {
           const int d = lane * MC + j - 2;
@@ -489,58 +528,51 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cblock_kernel(const __grid
       }
       CB_TS(i, 9);
       __syncthreads();  // [S3] U digits
-      CB_TS(i, 10);
 
-      // ---- P3b: U^m (x) C_i, four p-ranges per variable
-      if (pm_ < D) {
-        const int32_t* ub = ubuf + pm_ * (W + 4);
-        const int p0 = ppart * Wq, p1 = min(W, p0 + Wq);
-        int64_t x[MC], y[MC];
-        const int32_t* bq[MC];
-        int step[MC];
+      // ---- P3b: U^m (x) C_i, one warp per (variable, chunk of 16 digits of U)
+      for (int job = warp; job < D * nch; job += kWarps) {
+        const int jm = job / nch, ch = job - jm * nch;
+        const int p0 = ch * kPC;
+        const int4* up = (const int4*)(ubuf + jm * ustride + p0);
+        int32_t a[kPC];
 #pragma unroll
-        for (int j = 0; j < MC; j++) {
-          x[j] = 0;
-          y[j] = 0;
-          step[j] = okc[j] ? 1 : 0;
-          bq[j] = cbuf + (okc[j] ? lane * MC + j + Tc - p0 : -4);
+        for (int t4 = 0; t4 < kPC / 4; t4++) {
+          const int4 v = up[t4];
+          a[4 * t4] = v.x;
+          a[4 * t4 + 1] = v.y;
+          a[4 * t4 + 2] = v.z;
+          a[4 * t4 + 3] = v.w;
         }
-        int pp = p0;
-#pragma unroll 2
-        for (; pp + 1 < p1; pp += 2) {
-          const int32_t a0 = ub[pp], a1 = ub[pp + 1];
+        // x[j] = sum_t a[t] C[c_j + Tc - p0 - t], c_j = 3 lane + j: an 18-digit window of C_i
+        const int32_t* cp = cbuf + lane * MC + Tc - p0 - (kPC - 1);
+        int32_t cwin[kPC + MC - 1];
 #pragma unroll
-          for (int j = 0; j < MC; j++) {
-            x[j] = madw(a0, bq[j][0], x[j]);
-            y[j] = madw(a1, bq[j][-step[j]], y[j]);
-            bq[j] -= 2 * step[j];
-          }
-        }
-        if (pp < p1) {
-          const int32_t a0 = ub[pp];
+        for (int s2 = 0; s2 < kPC + MC - 1; s2++) cwin[s2] = cp[s2];
+        int64_t x[MC];
 #pragma unroll
-          for (int j = 0; j < MC; j++) x[j] = madw(a0, bq[j][0], x[j]);
-        }
+        for (int j = 0; j < MC; j++) x[j] = 0;
 #pragma unroll
-        for (int j = 0; j < MC; j++) xpart[(pm_ * kParts + ppart) * kCols + lane * MC + j] = x[j] + y[j];
-        if (mc && g == 0 && p1 > p0) {
-          mc->executed += (unsigned long long)(p1 - p0);
-          mc->useful += (unsigned long long)(p1 - p0) / 2 + 1;
+        for (int t = 0; t < kPC; t++)
+#pragma unroll
+          for (int j = 0; j < MC; j++) x[j] = madw(a[t], cwin[kPC - 1 - t + j], x[j]);
+#pragma unroll
+        for (int j = 0; j < MC; j++) xpart[job * kCols + lane * MC + j] = okc[j] ? x[j] : 0;
+        if (mc && g == 0) {
+          mc->executed += (unsigned long long)kPC;
+          mc->useful += (unsigned long long)kPC / 2 + 1;
         }
       }
       CB_TS(i, 11);
-      __syncthreads();  // [S4] partial product columns
-      CB_TS(i, 12);
+      __syncthreads();  // [S4] chunk vectors
 
       // ---- P3c: warp m rounds the new row
       if (target) {
         int64_t x[MC];
 #pragma unroll
-        for (int j = 0; j < MC; j++) {
-          int64_t s = 0;
+        for (int j = 0; j < MC; j++) x[j] = 0;
+        for (int ch = 0; ch < nch; ch++) {
 #pragma unroll
-          for (int pt = 0; pt < kParts; pt++) s += xpart[(m * kParts + pt) * kCols + lane * MC + j];
-          x[j] = s;
+          for (int j = 0; j < MC; j++) x[j] += xpart[(m * nch + ch) * kCols + lane * MC + j];
         }
         const Sd3 r = sd3(x[0], x[1], x[2], 1, W);
         ovf |= r.ovf != 0;
@@ -556,13 +588,27 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_cblock_kernel(const __grid
       }
       CB_TS(i, 13);
       __syncthreads();  // [S5] rows i+1 and their zero counts are visible
-      CB_TS(i, 14);
     }
 
     if (p.write_coef && g == 0) {
       int32_t* gcoef = p.coef + (size_t)traj * D * N1 * p.RS;
-      for (int r = warp; r < D * N1; r += kWarps)
-        for (int d = lane; d < p.RS; d += 32) gcoef[(size_t)r * p.RS + d] = d < W ? rows[r * stride + d] : 0;
+      // rows leave the kernel in canonical form: sd of the value the semi-normal digits hold
+#pragma unroll 1
+      for (int r = warp; r < D * N1; r += kWarps) {
+        int64_t cv[1][MC];
+        int32_t ce[1][MC];
+#pragma unroll
+        for (int j = 0; j < MC; j++) {
+          const int d = lane * MC + j - 2;
+          cv[0][j] = (d >= 0 && d < W) ? rows[r * stride + d] : 0;
+        }
+        wp::warp_sd<MC, false, 1>(cv, 1, W, ce);
+#pragma unroll
+        for (int j = 0; j < MC; j++) {
+          const int d = lane * MC + j - 2;
+          if (d >= 0 && d < p.RS) gcoef[(size_t)r * p.RS + d] = d < W ? ce[0][j] : 0;
+        }
+      }
     }
     // ---- state = RN_P(sum of the rows)
     if (target) {

@@ -9,7 +9,7 @@ const void* warp_fn_mc2(const Params& p);  // taylor_warp2.cu: two columns per l
 bool warp_supported(const Params& p) {
   const int gl = (p.D <= 3 && p.NP <= 2) ? 16 : 8;  // lanes per pair (warp_fn_mc)
   const int passes = (p.N + gl) / gl;               // products one lane accumulates per order
-  // passes x NU digit products of at most 2^54 each in one int64 column (< 2^63)
+  // passes x NU digit products of at most (2^27 + 1)^2 each (semi-normal digits) in one int64 column (< 2^63)
   return p.D <= kMaxD && p.all_q_small && p.NP <= wp::kMaxPairs && p.Lf + 3 <= wp::kMaxNU && p.Lf >= 3 &&
          passes * (p.Lf + 3) <= 500 && p.W <= 64;
 }

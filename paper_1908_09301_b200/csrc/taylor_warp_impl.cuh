@@ -224,6 +224,100 @@ __device__ __forceinline__ bool warp_sd(int64_t (&v)[NV][MC], int nv, int Wout, 
   return __any_sync(full, ovf);
 }
 
+// ---------------------------------------------------------------------------
+// The same value R = floor((V + [HALF] B^2/2) / B^2) in BALANCED SEMI-NORMAL digits:
+// e_j in [-B/2 - 1, B/2], sum_j e_j B^j = R exactly, three parallel carry rounds
+// and nothing else (no carry lookahead, no recoding). Every consumer of U and
+// of the coefficient rows is an exact integer product or sum, so only the VALUE
+// matters; the canonical digits (warp_sd of the same value) are produced when a
+// row leaves the kernel (compute_jet). Columns 0 and 1 are split by floor, so
+// after two rounds nothing more can leave them: the truncation is exact.
+template <int MC, bool HALF, int NV>
+__device__ __forceinline__ bool warp_bal(int64_t (&v)[NV][MC], int nv, int Wout, int32_t (&e)[NV][MC]) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  constexpr int32_t HB = (int32_t)(kRadix / 2);
+  bool istop[MC];
+  int32_t off[MC];
+#pragma unroll
+  for (int j = 0; j < MC; j++) {
+    const int c = lane * MC + j;
+    istop[j] = c == 32 * MC - 1;
+    off[j] = c < 2 ? 0 : HB;
+  }
+  int64_t tval[NV];
+  int32_t d1[NV][MC];
+  int64_t k1[NV][MC];
+#pragma unroll
+  for (int m = 0; m < NV; m++) {
+    tval[m] = 0;
+#pragma unroll
+    for (int j = 0; j < MC; j++) {
+      int64_t t = v[m][j] + off[j];
+      if (HALF && lane * MC + j == 1) t += HB;
+      if (istop[j]) tval[m] = v[m][j];
+      d1[m][j] = istop[j] ? 0 : (int32_t)((uint32_t)t & (uint32_t)kMask) - off[j];
+      k1[m][j] = istop[j] ? 0 : (t >> kRadixBits);
+    }
+  }
+  int64_t kin[NV];
+#pragma unroll
+  for (int m = 0; m < NV; m++) kin[m] = __shfl_up_sync(full, k1[m][MC - 1], 1);
+  // round 2 (carries < 2^35 in, < 2^8 out)
+  int32_t d2[NV][MC], k2[NV][MC];
+#pragma unroll
+  for (int m = 0; m < NV; m++) {
+#pragma unroll
+    for (int j = 0; j < MC; j++) {
+      const int64_t cin = j == 0 ? (lane == 0 ? 0ll : kin[m]) : k1[m][j - 1];
+      if (istop[j]) tval[m] += cin;
+      const int64_t t = (int64_t)d1[m][j] + cin + off[j];
+      d2[m][j] = istop[j] ? 0 : (int32_t)((uint32_t)t & (uint32_t)kMask) - off[j];
+      k2[m][j] = istop[j] ? 0 : (int32_t)(t >> kRadixBits);
+    }
+  }
+  int32_t kin2[NV];
+#pragma unroll
+  for (int m = 0; m < NV; m++) kin2[m] = __shfl_up_sync(full, k2[m][MC - 1], 1);
+  // round 3 (32 bits): carries in {-1, 0, 1} out
+  int32_t d3[NV][MC], k3[NV][MC];
+#pragma unroll
+  for (int m = 0; m < NV; m++) {
+#pragma unroll
+    for (int j = 0; j < MC; j++) {
+      const int32_t cin = j == 0 ? (lane == 0 ? 0 : kin2[m]) : k2[m][j - 1];
+      if (istop[j]) tval[m] += cin;
+      const int32_t t = d2[m][j] + cin + off[j];
+      d3[m][j] = istop[j] ? 0 : (int32_t)((uint32_t)t & (uint32_t)kMask) - off[j];
+      k3[m][j] = istop[j] ? 0 : (t >> kRadixBits);
+    }
+  }
+  int32_t kin3[NV];
+#pragma unroll
+  for (int m = 0; m < NV; m++) kin3[m] = __shfl_up_sync(full, k3[m][MC - 1], 1);
+  bool ovf = false;
+#pragma unroll
+  for (int m = 0; m < NV; m++) {
+#pragma unroll
+    for (int j = 0; j < MC; j++) {
+      const int c = lane * MC + j;
+      const int32_t cin = j == 0 ? (lane == 0 ? 0 : kin3[m]) : k3[m][j - 1];
+      int32_t ev;
+      if (istop[j]) {
+        tval[m] += cin;
+        ev = (int32_t)tval[m];
+        if (m < nv && (tval[m] > HB || tval[m] < -HB)) ovf = true;
+      } else {
+        ev = d3[m][j] + cin;
+      }
+      if (c < 2) ev = 0;
+      e[m][j] = ev;
+      if (m < nv && c - 2 >= Wout && ev != 0) ovf = true;
+    }
+  }
+  return __any_sync(full, ovf);
+}
+
 // leading zero digits of a row held across the lanes (digit d at column d + 2): Lf - top, W for a zero row
 template <int MC>
 __device__ __forceinline__ int lead_zeros(const int32_t (&e)[MC], int Lf) {
@@ -480,7 +574,7 @@ __global__ void __launch_bounds__(128, MINB) taylor_warp_kernel(const __grid_con
           const int d = lane * MC + j - 2;
           v[m][j] = (m < D && d >= 0 && d < W) ? st[m * p.RS + d] : 0;
         }
-      ovf |= warp_sd<MC, false, DT>(v, D, W, rowreg);
+      ovf |= warp_bal<MC, false, DT>(v, D, W, rowreg);
 #pragma unroll
       for (int m = 0; m < DT; m++) {
         if (m < D) {
@@ -535,12 +629,27 @@ __global__ void __launch_bounds__(128, MINB) taylor_warp_kernel(const __grid_con
               const int32_t* lb[MC];
 #pragma unroll
               for (int j = 0; j < MC; j++) lb[j] = lbuf + (size_t)slot * L.bw + (okc[j] ? lane * MC + j + T : -4);
-#pragma unroll 4
-              for (int pp = 0; pp < wa; pp++) {
-                const int32_t a = ar[pp];
+              // two accumulator chains: the IMAD.WIDE latency, not the pipe, bounds a lone warp
+              int64_t y[MC];
 #pragma unroll
-                for (int j = 0; j < MC; j++) U[m][j] = madw(a, lb[j][okc[j] ? -pp : 0], U[m][j]);
+              for (int j = 0; j < MC; j++) y[j] = 0;
+              int pp = 0;
+#pragma unroll 2
+              for (; pp + 1 < wa; pp += 2) {
+                const int32_t a0 = ar[pp], a1 = ar[pp + 1];
+#pragma unroll
+                for (int j = 0; j < MC; j++) {
+                  U[m][j] = madw(a0, lb[j][okc[j] ? -pp : 0], U[m][j]);
+                  y[j] = madw(a1, lb[j][okc[j] ? -pp - 1 : 0], y[j]);
+                }
               }
+              if (pp < wa) {
+                const int32_t a0 = ar[pp];
+#pragma unroll
+                for (int j = 0; j < MC; j++) U[m][j] = madw(a0, lb[j][okc[j] ? -pp : 0], U[m][j]);
+              }
+#pragma unroll
+              for (int j = 0; j < MC; j++) U[m][j] += y[j];
               if (mc) {
                 mc->executed += (unsigned long long)wa;
                 mc->useful += (unsigned long long)wa / 2 + 1;
@@ -569,7 +678,7 @@ __global__ void __launch_bounds__(128, MINB) taylor_warp_kernel(const __grid_con
       }
       // ---- U_i = rndb(...), digits to shared memory as [p][m]
       int32_t ureg[DT][MC];
-      ovf |= warp_sd<MC, true, DT>(U, D, W, ureg);
+      ovf |= warp_bal<MC, true, DT>(U, D, W, ureg);
 #pragma unroll
       for (int j = 0; j < MC; j++) {
         const int d = lane * MC + j - 2;
@@ -615,7 +724,7 @@ __global__ void __launch_bounds__(128, MINB) taylor_warp_kernel(const __grid_con
         mc->executed += (unsigned long long)W * D;
         mc->useful += (unsigned long long)(W / 2 + 1) * D;
       }
-      ovf |= warp_sd<MC, true, DT>(x, D, W, rowreg);
+      ovf |= warp_bal<MC, true, DT>(x, D, W, rowreg);
 #pragma unroll
       for (int m = 0; m < DT; m++) {
         if (m < D) {
@@ -634,9 +743,24 @@ __global__ void __launch_bounds__(128, MINB) taylor_warp_kernel(const __grid_con
 
     // ---- the jet, when asked for (compute_jet)
     if (p.write_coef) {
+      // rows leave the kernel in canonical form: sd of the value the semi-normal digits hold
       int32_t* gcoef = p.coef + (size_t)traj * D * N1 * p.RS;
-      for (int r = 0; r < D * N1; r++)
-        for (int d = lane; d < p.RS; d += 32) gcoef[(size_t)r * p.RS + d] = d < W ? rows[(size_t)r * L.stride + d] : 0;
+#pragma unroll 1
+      for (int r = 0; r < D * N1; r++) {
+        int64_t cv[1][MC];
+        int32_t ce[1][MC];
+#pragma unroll
+        for (int j = 0; j < MC; j++) {
+          const int d = lane * MC + j - 2;
+          cv[0][j] = (d >= 0 && d < W) ? rows[(size_t)r * L.stride + d] : 0;
+        }
+        warp_sd<MC, false, 1>(cv, 1, W, ce);
+#pragma unroll
+        for (int j = 0; j < MC; j++) {
+          const int d = lane * MC + j - 2;
+          if (d >= 0 && d < p.RS) gcoef[(size_t)r * p.RS + d] = d < W ? ce[0][j] : 0;
+        }
+      }
     }
     // ---- state = RN_P(sum of the rows)
 #pragma unroll

@@ -173,6 +173,31 @@ def test_block_kernel_bit_exact(gpu, K, N, steps, n_traj):
         assert np.array_equal(jets[j], FX.compute_jet(tables, fmt.frac_digits, N, states[j], **kw)), j
 
 
+@pytest.mark.parametrize("K,N,steps,n_traj,G", [(50, 40, 6, 1, 2), (100, 60, 4, 2, 4), (300, 100, 3, 1, 8), (500, 200, 2, 1, 16),
+                                                (500, 200, 1, 1, 8), (500, 200, 1, 1, 3), (700, 120, 2, 1, 16),
+                                                (500, 37, 3, 3, 5)])
+def test_cblock_kernel_bit_exact(gpu, K, N, steps, n_traj, G):
+    """One cluster of G CTAs per trajectory, rows in every CTA's shared memory, the
+    Cauchy sums split over CTAs, warps and lanes and all-gathered through DSMEM
+    (W <= 93 digits): records and the jet bit-exact vs the value-exact model,
+    whatever the cluster size (the partition cannot change a bit)."""
+    P = M.bits_for_digits(K)
+    ctx, system, fmt, tables = lorenz_tables(P, N)
+    base = [M.mp_from_decimal(t, ctx).as_fraction() for t in CANON_INIT]
+    states = np.stack([fmt.to_digits([b + Fraction(5 * j - 7, 10**18) for b in base]) for j in range(n_traj)])
+    with DevicePlan(tables, fmt, N, n_traj) as plan:
+        plan.configure("cblock", G)
+        assert plan.info()["kernel"] == "cblock"
+        _, r_gpu, status = plan.integrate(states, steps, 0, 1)
+        jets = plan.compute_jet(states)
+        kw = plan.model_kwargs()
+    assert kw == {"variant": 3} and not status.any()
+    for j in sorted({0, n_traj - 1}):
+        _, r_cpu = FX.integrate(tables, fmt.frac_digits, N, P, states[j], steps, 0, 1, **kw)
+        assert np.array_equal(r_gpu[:, j], r_cpu), j
+        assert np.array_equal(jets[j], FX.compute_jet(tables, fmt.frac_digits, N, states[j], **kw)), j
+
+
 def test_random_quadratic_systems_jets_bit_exact(golden, gpu):
     for name, c in golden.items():
         if not name.startswith("random_jet"):

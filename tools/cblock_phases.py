@@ -1,8 +1,9 @@
 """Phase timestamps (clock64, MPT_DEBUG) of the cblock kernel, rank 0, first step.
     python tools/cblock_phases.py K N G
-per order, warps 0 (target + units), 5 (product role), 15 (C_i loader): 0 order start, 1 zmin done, 2 side jobs done,
-3 units done, 4 after S1, 5 column sums written, 6 after the cluster barrier, 7 gather done, 8 after S2, 9 U rounded,
-10 after S3, 11 U x C partial, 12 after S4, 13 row rounded, 14 after S5
+per order, warps 0 (target + units), 8 (element sums + pushes), 13 (side warp with the non-integer linear product):
+0 order start, 1 zmin done, 2 side job done, 3 unit products done, 4 arrival at S1, 5 pushes issued, 6 after the cluster
+barrier, 7 U assembled, 9 U rounded, 11 U x C chunk done, 13 row rounded. Stamps taken right after a barrier are not
+reliable (the clock read is scheduled before the barrier resolves): read arrivals.
 """
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -34,6 +35,6 @@ for lo, hi in ((1, 8), (8, 32), (32, 64), (64, 128), (128, 256)):
     if not rr:
         continue
     print(f"orders {lo}-{hi}: order-to-order {np.mean([d[i + 1, 0, 0] - d[i, 0, 0] for i in rr]):.0f}")
-    for w, name in ((0, "w0 "), (1, "w5 "), (2, "w15")):
+    for w, name in ((0, "w0 "), (1, "w8 "), (2, "w13")):
         row = [np.mean([d[i, w, k] - d[i, 0, 0] for i in rr if d[i, w, k] > 0] or [0]) for k in range(15)]
         print(f"  {name}: " + " ".join(f"{x:6.0f}" for x in row))
