@@ -168,7 +168,7 @@ static int choose_kernel(mpt_plan* pl, int kernel, int want) {
   if (kernel == 9 && pl->have_constants &&
       mpt::cblock_supported(p)) {
     for (int G : tries) {
-      if (G > want || G < 2) continue;
+      if (G > want) continue;
       const size_t s = mpt::cblock_smem_bytes(p, G);
       if (s > (size_t)pl->optin) continue;
       if (mpt::cblock_max_clusters(p, s, G) < 1) continue;

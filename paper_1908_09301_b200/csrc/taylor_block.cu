@@ -11,8 +11,9 @@
 // shuffle reduce-scatter per warp. What changes is the width: four warps per
 // product pair take k = l, l + 128, ...; each warp leaves its reduced columns
 // in shared memory; after one CTA barrier warp m assembles U^m from the four
-// partial column vectors of every pair, rounds it, multiplies by C_i and rounds
-// the new row; a second barrier publishes the rows. Two CTA barriers per order.
+// partial column vectors of every pair and rounds it; U^m (x) C_i is cut into
+// chunks of 32 digits of U, one warp per (variable, chunk), operands in registers;
+// warp m sums the chunk vectors and rounds the new row. Four CTA barriers per order.
 #include "taylor_warp_impl.cuh"
 
 namespace mpt {
@@ -27,10 +28,13 @@ constexpr int MC = 2;        // columns per lane (Lf + 4 <= 64)
 constexpr int DT = 3;        // variables, one target warp each
 constexpr int kPairWarps = 4;
 constexpr int kPartCols = 68;  // 64 reduced columns + the carry out of the top one
+constexpr int kPC = 32;        // digits of U per chunk of the U (x) C_i product (one warp per variable and chunk)
+constexpr int kCLo = 36;       // zero digits below digit 0 of the staged C_i
+constexpr int kCols = 32 * MC;
 
 struct Layout {
-  int ncols, stride, nrows, bw, sw, nbig;
-  size_t off_rows, off_zt, off_bbuf, off_lbuf, off_ubuf, off_part, off_scr, off_st, total;
+  int ncols, stride, nrows, bw, sw, nbig, nch, ustride;
+  size_t off_rows, off_zt, off_bbuf, off_lbuf, off_ubuf, off_part, off_xpart, off_lpart, off_scr, off_st, total;
 };
 
 __host__ __device__ inline Layout make_layout(const Params& p) {
@@ -38,9 +42,11 @@ __host__ __device__ inline Layout make_layout(const Params& p) {
   L.ncols = p.Lf + 4;
   L.stride = (kLo + p.W) | 1;
   L.nrows = p.D * (p.N + 1);
-  L.bw = 4 + p.W + p.Lf + 4;
+  L.bw = kCLo + p.W + p.Lf + 8;  // zero-padded constant operand of the chunked products
   L.sw = p.W + 3;
   L.nbig = wp::n_big_lin(p);
+  L.nch = (p.W + kPC - 1) / kPC;
+  L.ustride = kPC * L.nch + 4;
   size_t o = 0;
   auto take = [&](size_t bytes) {
     size_t r = o;
@@ -51,8 +57,10 @@ __host__ __device__ inline Layout make_layout(const Params& p) {
   L.off_zt = take((size_t)L.nrows);
   L.off_bbuf = take(sizeof(int32_t) * (size_t)L.bw);
   L.off_lbuf = take(sizeof(int32_t) * (size_t)L.bw * L.nbig);
-  L.off_ubuf = take(sizeof(int32_t) * (size_t)DT * (p.W + 4));
+  L.off_ubuf = take(sizeof(int32_t) * (size_t)DT * L.ustride);
   L.off_part = take(sizeof(int64_t) * 2 * kPairWarps * kPartCols);
+  L.off_xpart = take(sizeof(int64_t) * (size_t)DT * L.nch * kCols);
+  L.off_lpart = take(sizeof(int64_t) * (size_t)(L.nbig > 0 ? DT * L.nch * kCols : 0));
   L.off_scr = take(sizeof(int64_t) * (size_t)p.D * L.sw);
   L.off_st = take(sizeof(int32_t) * (size_t)p.D * p.RS + sizeof(int2) * kMaxD);
   L.total = o;
@@ -169,10 +177,12 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_block_kernel(const __grid_
   const Layout L = make_layout(p);
   int32_t* rows = (int32_t*)(smem + L.off_rows) + kLo;
   uint8_t* zt = (uint8_t*)(smem + L.off_zt);
-  int32_t* bbuf = (int32_t*)(smem + L.off_bbuf) + 4;
-  int32_t* lbuf = (int32_t*)(smem + L.off_lbuf) + 4;
+  int32_t* bbuf = (int32_t*)(smem + L.off_bbuf) + kCLo;
+  int32_t* lbuf = (int32_t*)(smem + L.off_lbuf) + kCLo;
   int32_t* ubuf = (int32_t*)(smem + L.off_ubuf);
   int64_t* part = (int64_t*)(smem + L.off_part);
+  int64_t* xpart = (int64_t*)(smem + L.off_xpart);
+  int64_t* lpart = (int64_t*)(smem + L.off_lpart);
   int64_t* scr = (int64_t*)(smem + L.off_scr);
   int32_t* st = (int32_t*)(smem + L.off_st);
   int2* stinfo = (int2*)(st + (size_t)p.D * p.RS);
@@ -242,6 +252,41 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_block_kernel(const __grid_
       }
   }
 
+  // linear-product role (phase 1): warp 7 - job computes one 32-digit chunk of the non-integer
+  // linear products of one equation (D equations x nch <= 2 chunks <= 6 jobs)
+  int job_m = -1, job_ch = 0;
+  unsigned jobmask = 0;
+  int jobslot[DT];
+  {
+    const int jw = kWarps - 1 - warp;
+    int nb = 0;
+    for (int mm = 0; mm < D; mm++) {
+      bool big = false;
+      for (int t = 0; t < D; t++) big |= !p.lin_small[mm * D + t];
+      if (big) {
+        if (jw / L.nch == nb) {
+          job_m = mm;
+          job_ch = jw % L.nch;
+        }
+        nb++;
+      }
+    }
+    int slot = 0;
+    for (int e = 0; e < D * D; e++) {
+      if (p.lin_small[e]) continue;
+#pragma unroll
+      for (int t = 0; t < DT; t++)
+        if (job_m >= 0 && e / D == job_m && e % D == t) {
+          jobmask |= 1u << t;
+          jobslot[t] = slot;
+        }
+      slot++;
+    }
+#pragma unroll
+    for (int t = 0; t < DT; t++)
+      if (!(jobmask & (1u << t))) jobslot[t] = 0;
+  }
+
   wp::Ctx cx{rows, zt, L.stride, N1, Lf, p.NP};
   MacCount mcount;
   MacCount* mc = p.counters ? &mcount : nullptr;
@@ -279,6 +324,36 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_block_kernel(const __grid_
           if (q < p.NP) z = min(z, (int)zt[p.pj[q] * N1 + i - k] + (int)zt[p.pk[q] * N1 + k]);
       const int zmin = __reduce_min_sync(full, z);
       const int nureal = Lf + 3 - zmin, ctop = Lf + 2 - zmin;
+      if (job_m >= 0) {
+        // tprod(lin[job_m][t], a~_i^t), digits p0 .. p0+31 of the row: operands in registers
+        const int p0 = job_ch * kPC;
+        int64_t x[MC];
+#pragma unroll
+        for (int j = 0; j < MC; j++) x[j] = 0;
+#pragma unroll
+        for (int t = 0; t < DT; t++) {
+          if (jobmask & (1u << t)) {
+            const int32_t* ar = rows + (size_t)(t * N1 + i) * L.stride + p0;
+            int32_t a[kPC];
+#pragma unroll
+            for (int tt = 0; tt < kPC; tt++) a[tt] = p0 + tt < W ? ar[tt] : 0;
+            const int32_t* cp = lbuf + (size_t)jobslot[t] * L.bw + lane * MC + T - p0 - (kPC - 1);
+            int32_t cwin[kPC + MC - 1];
+#pragma unroll
+            for (int s2 = 0; s2 < kPC + MC - 1; s2++) cwin[s2] = cp[s2];
+#pragma unroll
+            for (int tt = 0; tt < kPC; tt++)
+#pragma unroll
+              for (int j = 0; j < MC; j++) x[j] = madw(a[tt], cwin[kPC - 1 - tt + j], x[j]);
+            if (mc) {
+              mc->executed += (unsigned long long)kPC;
+              mc->useful += (unsigned long long)kPC / 2 + 1;
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < MC; j++) lpart[(size_t)(job_m * L.nch + job_ch) * kCols + lane * MC + j] = okc[j] ? x[j] : 0;
+      }
       if (pq < p.NP && nureal > 0)
         cauchy_dispatch(cx, va, vb, i, zmin, kl, part + (size_t)warp * kPartCols, mc);
       if (warp == kWarps - 1) {  // C_i into the padded operand buffer
@@ -315,72 +390,68 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_block_kernel(const __grid_
           }
           U[0][j] = s;
         }
-        if (bigmask) {
+        if (bigmask) {  // the chunk vectors of the non-integer linear products (phase 1)
+          for (int ch = 0; ch < L.nch; ch++) {
 #pragma unroll
-          for (int t = 0; t < DT; t++) {
-            if (bigmask & (1u << t)) {
-              const int32_t* ar = rows + (size_t)(t * N1 + i) * L.stride;
-              const int wa = W - zt[t * N1 + i];
-              const int32_t* lb[MC];
-#pragma unroll
-              for (int j = 0; j < MC; j++) lb[j] = lbuf + (size_t)bigslot[t] * L.bw + (okc[j] ? lane * MC + j + T : -4);
-#pragma unroll 4
-              for (int pp = 0; pp < wa; pp++) {
-                const int32_t a = ar[pp];
-#pragma unroll
-                for (int j = 0; j < MC; j++) U[0][j] = madw(a, lb[j][okc[j] ? -pp : 0], U[0][j]);
-              }
-              if (mc) {
-                mc->executed += (unsigned long long)wa;
-                mc->useful += (unsigned long long)wa / 2 + 1;
-              }
-            }
+            for (int j = 0; j < MC; j++) U[0][j] += lpart[(size_t)(m * L.nch + ch) * kCols + lane * MC + j];
           }
         }
         int32_t ureg[1][MC];
         ovf |= wp::warp_bal<MC, true, 1>(U, 1, W, ureg);
-        int32_t* ub = ubuf + (size_t)m * (W + 4);
+        int32_t* ub = ubuf + (size_t)m * L.ustride;
 #pragma unroll
         for (int j = 0; j < MC; j++) {
           const int d = lane * MC + j - 2;
           if (d >= 0 && d < W) ub[d] = ureg[0][j];
         }
-        __syncwarp();
+      }
+      __syncthreads();  // [A2] U digits
+
+      // ---- phase 2b: U^m (x) C_i in chunks of 32 digits of U, one warp per (variable, chunk):
+      // operands in registers, fully unrolled (a lone warp pays ~5 cycles per instruction, so the
+      // product is spread over the warps that would otherwise wait)
+      for (int job = warp; job < D * L.nch; job += kWarps) {
+        const int jm = job / L.nch, ch = job - jm * L.nch;
+        const int p0 = ch * kPC;
+        const int4* up = (const int4*)(ubuf + (size_t)jm * L.ustride + p0);
+        int32_t a[kPC];
+#pragma unroll
+        for (int t4 = 0; t4 < kPC / 4; t4++) {
+          const int4 v4 = up[t4];
+          a[4 * t4] = v4.x;
+          a[4 * t4 + 1] = v4.y;
+          a[4 * t4 + 2] = v4.z;
+          a[4 * t4 + 3] = v4.w;
+        }
+        // x[j] = sum_t a[t] C[c_j + Tc - p0 - t], c_j = MC lane + j: a (kPC + MC - 1)-digit window of C_i
+        const int32_t* cp = bbuf + lane * MC + Tc - p0 - (kPC - 1);
+        int32_t cwin[kPC + MC - 1];
+#pragma unroll
+        for (int s2 = 0; s2 < kPC + MC - 1; s2++) cwin[s2] = cp[s2];
+        int64_t x[MC];
+#pragma unroll
+        for (int j = 0; j < MC; j++) x[j] = 0;
+#pragma unroll
+        for (int t = 0; t < kPC; t++)
+#pragma unroll
+          for (int j = 0; j < MC; j++) x[j] = madw(a[t], cwin[kPC - 1 - t + j], x[j]);
+#pragma unroll
+        for (int j = 0; j < MC; j++) xpart[(size_t)job * kCols + lane * MC + j] = okc[j] ? x[j] : 0;
+        if (mc) {
+          mc->executed += (unsigned long long)kPC;
+          mc->useful += (unsigned long long)kPC / 2 + 1;
+        }
+      }
+      __syncthreads();  // [A3] chunk vectors
+
+      // ---- phase 2c: warp m rounds the new row
+      if (target) {
         int64_t x[1][MC];
-        {
-          const int32_t* bq[MC];
-          int step[MC];
 #pragma unroll
-          for (int j = 0; j < MC; j++) {
-            x[0][j] = 0;
-            bq[j] = bbuf + (okc[j] ? lane * MC + j + Tc : -4);
-            step[j] = okc[j] ? 1 : 0;
-          }
-          int64_t y[MC];  // second accumulator chain (IMAD.WIDE latency is ~15 cycles)
+        for (int j = 0; j < MC; j++) x[0][j] = 0;
+        for (int ch = 0; ch < L.nch; ch++) {
 #pragma unroll
-          for (int j = 0; j < MC; j++) y[j] = 0;
-          int pp = 0;
-#pragma unroll 2
-          for (; pp + 1 < W; pp += 2) {
-            const int32_t a0 = ub[pp], a1 = ub[pp + 1];
-#pragma unroll
-            for (int j = 0; j < MC; j++) {
-              x[0][j] = madw(a0, bq[j][0], x[0][j]);
-              y[j] = madw(a1, bq[j][-step[j]], y[j]);
-              bq[j] -= 2 * step[j];
-            }
-          }
-          if (pp < W) {
-            const int32_t a0 = ub[pp];
-#pragma unroll
-            for (int j = 0; j < MC; j++) x[0][j] = madw(a0, bq[j][0], x[0][j]);
-          }
-#pragma unroll
-          for (int j = 0; j < MC; j++) x[0][j] += y[j];
-          if (mc) {
-            mc->executed += (unsigned long long)W;
-            mc->useful += (unsigned long long)W / 2 + 1;
-          }
+          for (int j = 0; j < MC; j++) x[0][j] += xpart[(size_t)(m * L.nch + ch) * kCols + lane * MC + j];
         }
         int32_t rowreg[1][MC];
         ovf |= wp::warp_bal<MC, true, 1>(x, 1, W, rowreg);
