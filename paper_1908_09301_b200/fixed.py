@@ -38,6 +38,9 @@ def _round_div(num: int, den: int) -> int:
     return q
 
 
+_CTAB_CACHE: dict = {}  # (frac_bits, width, step, order) -> read-only digit table
+
+
 @dataclass(frozen=True)
 class FixedFormat:
     prec_bits: int
@@ -143,4 +146,15 @@ class FixedFormat:
         return [_round_div(num, den * (i + 1)) for i in range(order)]
 
     def ctab(self, scale: Fraction, order: int) -> np.ndarray:
-        return self.ints_to_digits(self.ctab_ints(scale, order))
+        """The tau/(i+1) digit table; memoised per (format, step, order): at K = 4200,
+        N = 3500 it is 3500 divisions of 14 000-bit integers, repeated by every
+        integrate() call on the same step size otherwise."""
+        key = (self.frac_bits, self.width, Fraction(scale), order)
+        hit = _CTAB_CACHE.get(key)
+        if hit is None:
+            hit = self.ints_to_digits(self.ctab_ints(scale, order))
+            hit.setflags(write=False)
+            if len(_CTAB_CACHE) >= 16:
+                _CTAB_CACHE.pop(next(iter(_CTAB_CACHE)))
+            _CTAB_CACHE[key] = hit
+        return hit
