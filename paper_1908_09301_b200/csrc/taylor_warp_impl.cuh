@@ -318,6 +318,17 @@ __device__ __forceinline__ bool warp_bal(int64_t (&v)[NV][MC], int nv, int Wout,
   return __any_sync(full, ovf);
 }
 
+// the rounding the kernels use inside their loops (MPT_CANONICAL_ROUNDING: the canonical
+// digits everywhere, for A/B timing of the semi-normal representation)
+template <int MC, bool HALF, int NV>
+__device__ __forceinline__ bool warp_rnd(int64_t (&v)[NV][MC], int nv, int Wout, int32_t (&e)[NV][MC]) {
+#ifdef MPT_CANONICAL_ROUNDING
+  return warp_sd<MC, HALF, NV>(v, nv, Wout, e);
+#else
+  return warp_bal<MC, HALF, NV>(v, nv, Wout, e);
+#endif
+}
+
 // leading zero digits of a row held across the lanes (digit d at column d + 2): Lf - top, W for a zero row
 template <int MC>
 __device__ __forceinline__ int lead_zeros(const int32_t (&e)[MC], int Lf) {
@@ -574,7 +585,7 @@ __global__ void __launch_bounds__(128, MINB) taylor_warp_kernel(const __grid_con
           const int d = lane * MC + j - 2;
           v[m][j] = (m < D && d >= 0 && d < W) ? st[m * p.RS + d] : 0;
         }
-      ovf |= warp_bal<MC, false, DT>(v, D, W, rowreg);
+      ovf |= warp_rnd<MC, false, DT>(v, D, W, rowreg);
 #pragma unroll
       for (int m = 0; m < DT; m++) {
         if (m < D) {
@@ -678,7 +689,7 @@ __global__ void __launch_bounds__(128, MINB) taylor_warp_kernel(const __grid_con
       }
       // ---- U_i = rndb(...), digits to shared memory as [p][m]
       int32_t ureg[DT][MC];
-      ovf |= warp_bal<MC, true, DT>(U, D, W, ureg);
+      ovf |= warp_rnd<MC, true, DT>(U, D, W, ureg);
 #pragma unroll
       for (int j = 0; j < MC; j++) {
         const int d = lane * MC + j - 2;
@@ -724,7 +735,7 @@ __global__ void __launch_bounds__(128, MINB) taylor_warp_kernel(const __grid_con
         mc->executed += (unsigned long long)W * D;
         mc->useful += (unsigned long long)(W / 2 + 1) * D;
       }
-      ovf |= warp_bal<MC, true, DT>(x, D, W, rowreg);
+      ovf |= warp_rnd<MC, true, DT>(x, D, W, rowreg);
 #pragma unroll
       for (int m = 0; m < DT; m++) {
         if (m < D) {
