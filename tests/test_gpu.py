@@ -198,6 +198,47 @@ def test_cblock_kernel_bit_exact(gpu, K, N, steps, n_traj, G):
         assert np.array_equal(jets[j], FX.compute_jet(tables, fmt.frac_digits, N, states[j], **kw)), j
 
 
+def _mixed_system(ctx):
+    """dx/dt = 1/3 + 10.5 (y - x) + 0.7 z,  dy/dt = 28 x - 1.25 y - x z,  dz/dt = -1/7 + 0.3 x - 8/3 z + x y:
+    two integer-coefficient pairs, a non-integer linear coefficient in every equation (two in the
+    first and the last), non-zero constants."""
+    def v(t):
+        return M.mp_from_decimal(t, ctx) if "/" not in t else ctx.div(M.mp_from_decimal(t.split("/")[0], ctx),
+                                                                       M.mp_from_decimal(t.split("/")[1], ctx))
+    z = M.mp_from_decimal("0", ctx)
+    return M.QuadraticODESystem(
+        dim=3,
+        constant=(v("1/3"), z, v("-1/7")),
+        linear=((v("-10.5"), v("10.5"), v("0.7")), (v("28"), v("-1.25"), z), (v("0.3"), z, v("-8/3"))),
+        bilinear=((), (M.BilinearTerm(0, 2, M.mp_from_decimal("-1", ctx)),), (M.BilinearTerm(0, 1, M.mp_from_decimal("1", ctx)),)),
+    )
+
+
+@pytest.mark.parametrize("kernel,cluster,K,N,steps", [("warp", 1, 100, 40, 5), ("warp", 1, 250, 60, 2), ("block", 1, 300, 60, 3),
+                                                       ("block", 1, 450, 50, 2), ("cblock", 4, 300, 60, 3),
+                                                       ("cblock", 16, 500, 70, 2), ("cblock", 1, 120, 30, 3)])
+def test_value_exact_kernels_general_linear_terms(gpu, kernel, cluster, K, N, steps):
+    """The chunked / side-warp products of the non-integer linear coefficients (several per
+    system, in every equation) in the warp, block and cblock kernels: records and jet bit-exact
+    vs the value-exact model."""
+    P = M.bits_for_digits(K)
+    ctx = M.PrecisionContext(P)
+    system = _mixed_system(ctx)
+    fmt = FixedFormat(P)
+    tables = SystemTables.build(system, fmt, N, Fraction(1, 128))
+    st = fmt.to_digits([M.mp_from_decimal(t, ctx) for t in ("1.5", "-2.25", "3.125")])
+    with DevicePlan(tables, fmt, N, 1) as plan:
+        plan.configure(kernel, cluster)
+        assert plan.info()["kernel"] == kernel
+        _, r_gpu, status = plan.integrate(st, steps, 0, 1)
+        jet = plan.compute_jet(st)[0]
+        kw = plan.model_kwargs()
+    assert kw == {"variant": 3} and not status.any()
+    _, r_cpu = FX.integrate(tables, fmt.frac_digits, N, P, st, steps, 0, 1, **kw)
+    assert np.array_equal(r_gpu[:, 0], r_cpu)
+    assert np.array_equal(jet, FX.compute_jet(tables, fmt.frac_digits, N, st, **kw))
+
+
 def test_random_quadratic_systems_jets_bit_exact(golden, gpu):
     for name, c in golden.items():
         if not name.startswith("random_jet"):
