@@ -1060,6 +1060,28 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
       asm volatile("cp.async.wait_all;" ::: "memory");
       __syncthreads();
 
+      // column-sum pass: this thread's first item (target, column) and the bilinear terms of a
+      // U target are the same for every order -- out of the loop (runtime-indexed constant-bank
+      // loads and the division cost the single-issue critical path ~1 K cycles per order)
+      const int cs_ntg = 2 * p.D;
+      const bool cs_on = tid < cs_ntg * g.ncols;
+      const int cs_tg = cs_on ? tid / g.ncols : 0, cs_c = cs_on ? tid - cs_tg * g.ncols : 0;
+      int cs_nt = 0, cs_q[4] = {0, 0, 0, 0}, cs_coef[4] = {0, 0, 0, 0};
+      bool cs_many = false;  // more than four terms in one equation: the generic loop
+      if (cs_on && cs_tg < p.D)
+        for (int t = 0; t < p.NT; t++)
+          if (p.teq[t] == cs_tg) {
+            if (cs_nt < 4) {
+              cs_q[cs_nt] = p.tpair[t];
+              cs_coef[cs_nt] = p.tq_int[t];
+              cs_nt++;
+            } else {
+              cs_many = true;
+            }
+          }
+      cs_many = __syncthreads_or(cs_many) != 0;
+      int ssum_lag = 0;  // rows of the previous order still to be added to the state sum (aux warp)
+
       for (int i = 0; i < N; i++) {
         const int par = i & 1, j = i + 1;
         const bool tlog = p.dbg && n == p.start_step + 1 && i < 256 && lane == 0;
@@ -1119,7 +1141,15 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
             }
           }
         } else {
-          // aux warp: wait for the bulk CTAs' L'(j) (gathered in the column-sum pass below)
+          // aux warp: the rows rounded at the previous order join the state sum here, off the
+          // row warps' critical path (their buffer is rewritten two orders later)
+          if (ssum_lag) {
+            for (int m = 0; m < p.D; m++) {
+              const int32_t* rw = LR(R_ROW + par * p.D + m);
+              for (int d = lane; d < p.W; d += 32) ssum[(size_t)m * (p.W + 3) + d] += rw[d];
+            }
+          }
+          // wait for the bulk CTAs' L'(j) (gathered in the column-sum pass below)
           const bool have = doU && j >= 4 && p.NP > 0;
           if (have) {
             const int rp = j & 1;
@@ -1134,22 +1164,36 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
         // ---- column sums of every target on all warps, then the roundings:
         //      U_j^m (warps 0..D-1), rows a~_{i+1}^m (warps D..2D-1)
         {
-          const int ntg = 2 * p.D;
+          const int ntg = cs_ntg;
           for (int e = tid; e < ntg * g.ncols; e += kThreads) {
-            const int tg = e / g.ncols, c = e - tg * g.ncols;
+            const bool firstitem = e == tid;
+            const int tg = firstitem ? cs_tg : e / g.ncols, c = firstitem ? cs_c : e - tg * g.ncols;
             const bool isU = tg < p.D;
             if (isU && !doU) continue;
             const int k0 = s_tr[lk][tg], k1 = s_tr[lk][tg + 1];
             int64_t sacc = 0;
             if (isU && doU && j >= 4 && p.NP > 0) {  // q_t * sum over the bulk CTAs of L'_t(j)
               const int64_t* rv = recv + (size_t)(j & 1) * Gb * NPp * g.ncp;
-              for (int t = 0; t < p.NT; t++) {
-                if (p.teq[t] != tg) continue;
-                const int q = p.tpair[t];
-                int64_t v = 0;
+              if (firstitem && !cs_many) {
+#pragma unroll
+                for (int tt = 0; tt < 4; tt++) {
+                  if (tt < cs_nt) {
+                    const int64_t* rq = rv + (size_t)cs_q[tt] * g.ncp + c;
+                    int64_t v = 0;
 #pragma unroll 5
-                for (int r = 0; r < Gb; r++) v += rv[((size_t)r * NPp + q) * g.ncp + c];
-                sacc += (int64_t)p.tq_int[t] * v;
+                    for (int r = 0; r < Gb; r++) v += rq[(size_t)r * NPp * g.ncp];
+                    sacc += (int64_t)cs_coef[tt] * v;
+                  }
+                }
+              } else {
+                for (int t = 0; t < p.NT; t++) {
+                  if (p.teq[t] != tg) continue;
+                  const int q = p.tpair[t];
+                  int64_t v = 0;
+#pragma unroll 5
+                  for (int r = 0; r < Gb; r++) v += rv[((size_t)r * NPp + q) * g.ncp + c];
+                  sacc += (int64_t)p.tq_int[t] * v;
+                }
               }
             }
             for (int k = k0; k < k1; k++) sacc += (int64_t)s_pl[lk][k].w * cpart[(size_t)k * g.ncp + c];
@@ -1170,7 +1214,6 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
             if (!isU) {  // row a~_j: publish, state sum, keep row 1
               __syncwarp();
               push_row(m, j, LR(rr));
-              for (int d = lane; d < p.W; d += 32) ssum[(size_t)m * (p.W + 3) + d] += LR(rr)[d];
               if (i == 0) {
                 for (int d = lane; d < p.W; d += 32) LR(R_ROW1 + m)[d] = LR(rr)[d];
                 if (lane == 0) linfo[R_ROW1 + m] = linfo[rr];
@@ -1183,7 +1226,15 @@ __global__ void __launch_bounds__(kThreads, 1) taylor_mx_kernel(const __grid_con
         LT(4);
         __syncthreads();
         LT(5);
+        ssum_lag = 1;
 #undef LT
+      }
+      // the rows of the last order (buffer (N & 1))
+      if (warp == kWarps - 1 && N > 0) {
+        for (int m = 0; m < p.D; m++) {
+          const int32_t* rw = LR(R_ROW + (N & 1) * p.D + m);
+          for (int d = lane; d < p.W; d += 32) ssum[(size_t)m * (p.W + 3) + d] += rw[d];
+        }
       }
       if (lane == 0) bulk_wait_read();
       __syncthreads();
