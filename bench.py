@@ -18,7 +18,7 @@ N > 1 ranks: under torchrun the RANK/WORLD_SIZE environment is used; started
 plainly (`python bench.py --gpus N`) the script spawns its own N ranks on
 127.0.0.1.
 
-Outputs one JSON line (rank 0). See DESIGN.md §6 for every field.
+Outputs one JSON line (rank 0). See DESIGN.md §5 for every field.
 """
 
 from __future__ import annotations
