@@ -40,15 +40,17 @@ METRIC = "Lorenz Taylor steps/sec at (N,K) and limb-MAC/s as fraction of INT roo
 INIT = ("-15.8", "-17.48", "35.64")
 
 # name -> (K digits, order N, tau, trajectories per GPU, default Taylor steps per bench step, label)
+# (ensemble launches are long enough to be past the start-up transient: the first steps from the canonical
+# initial condition are 10-15 % cheaper than the sustained rate)
 WORKLOADS = {
     "k50": (50, 40, "0.01", 1, 100, "configs[0]: K=50 N=40 tau=0.01, single trajectory"),
     "k500": (500, 200, "0.01", 1, 100, "configs[1]: K=500 N=200 tau=0.01, single trajectory"),
     "k2200": (2200, 1000, "0.01", 1, 5, "configs[2]: K=2200 N=1000 tau=0.01, single trajectory"),
     "k4200": (4200, 3500, "0.01", 1, 1, "configs[3]: K=4200 N=3500 tau=0.01, single trajectory"),
-    "ens100": (100, 60, "0.01", 4096, 10, "configs[4]: ensemble M=4096 at (K,N)=(100,60)"),
-    "ens200": (200, 120, "0.01", 4096, 5, "configs[4]: ensemble M=4096 at (K,N)=(200,120)"),
-    "ens400": (400, 240, "0.01", 4096, 2, "configs[4]: ensemble M=4096 at (K,N)=(400,240)"),
-    "ens800": (800, 480, "0.01", 4096, 1, "configs[4]: ensemble M=4096 at (K,N)=(800,480)"),
+    "ens100": (100, 60, "0.01", 4096, 100, "configs[4]: ensemble M=4096 at (K,N)=(100,60)"),
+    "ens200": (200, 120, "0.01", 4096, 50, "configs[4]: ensemble M=4096 at (K,N)=(200,120)"),
+    "ens400": (400, 240, "0.01", 4096, 20, "configs[4]: ensemble M=4096 at (K,N)=(400,240)"),
+    "ens800": (800, 480, "0.01", 4096, 2, "configs[4]: ensemble M=4096 at (K,N)=(800,480)"),
 }
 
 
